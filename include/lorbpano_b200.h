@@ -1,0 +1,258 @@
+/* lorbpano_b200.h — C-ABI of the B200-native stitching hot path.
+ *
+ * This is the drop-in boundary under the reference's C++ API
+ * (/root/reference/proj/include/lorbpano/*.hpp). Every entry point names the
+ * reference function it replaces (file:line, relative to proj/include/lorbpano/).
+ * The C++ drop-in headers (paper_1810_03988_b200/include/lorbpano/) forward to
+ * these functions and re-throw lp_status codes as the matching lorbpano::Error
+ * subclass, so the reference's callers (StitchEngine stage bodies, CLI, tests)
+ * keep their exception behaviour.
+ *
+ * Conventions
+ *  - plain pointers + sizes, no C++ or torch types;
+ *  - every pixel/feature pointer may be HOST or DEVICE memory (detected with
+ *    cudaPointerGetAttributes); host buffers are staged through the context's
+ *    device arena;
+ *  - outputs go to caller buffers with an explicit capacity and a count out-param;
+ *  - errors are returned as lp_status, never thrown across the ABI;
+ *    lp_last_error() gives the message (thread-local);
+ *  - images are row-major, interleaved channels (Raster<T>, image.hpp:22-60);
+ *  - descriptors are packed as 2*W uint64 words per descriptor, W = ceil(n_d/64):
+ *    gt[0..W) then lt[0..W) (Descriptor, lorb.hpp:45-69, without the n_d field).
+ */
+#ifndef LORBPANO_B200_H
+#define LORBPANO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* 0 = ok; 1..28 mirror the error.hpp:19-56 declaration order. */
+typedef enum lp_status {
+    LP_OK = 0,
+    LP_FILE_NOT_FOUND = 1,
+    LP_UNSUPPORTED_FORMAT = 2,
+    LP_CORRUPT_DATA = 3,
+    LP_INVALID_SIGMA = 4,
+    LP_IMAGE_TOO_SMALL = 5,
+    LP_BAD_TARGET_DIMS = 6,
+    LP_NO_OVERLAP = 7,
+    LP_OVERLAP_EXCEEDS_IMAGE = 8,
+    LP_REGION_TOO_SMALL = 9,
+    LP_WINDOW_OUT_OF_BOUNDS = 10,
+    LP_PATCH_OUT_OF_BOUNDS = 11,
+    LP_LENGTH_MISMATCH = 12,
+    LP_BAD_PARAMS = 13,
+    LP_TOO_MANY_PROBES = 14,
+    LP_PARAM_MISMATCH = 15,
+    LP_EMPTY_INPUT = 16,
+    LP_DEGENERATE_CONFIGURATION = 17,
+    LP_NUMERICAL_FAILURE = 18,
+    LP_INSUFFICIENT_MATCHES = 19,
+    LP_NO_MODEL_FOUND = 20,
+    LP_SINGULAR_HOMOGRAPHY = 21,
+    LP_MASK_MISMATCH = 22,
+    LP_TOO_MANY_LEVELS = 23,
+    LP_CAPACITY_OVERFLOW = 24,
+    LP_NO_VALID_HOMOGRAPHY_YET = 25,
+    LP_PARSE_ERROR = 26,
+    LP_VALIDATION_ERROR = 27,
+    LP_MISSING_FRAMES = 28,
+    LP_CUDA_ERROR = 100,
+    LP_NO_DEVICE = 101,
+    LP_INTERNAL = 102
+} lp_status;
+
+/* ---- POD mirrors (layouts identical to the reference structs on x86-64) ---- */
+
+/* DetectionRegion, lorb.hpp:25-32 (20 B) */
+typedef struct lp_region { int x0, y0, x1, y1, camera_id; } lp_region;
+/* Keypoint, lorb.hpp:17-22 (16 B) */
+typedef struct lp_keypoint { int x, y; float response; int region_id; } lp_keypoint;
+/* BriefPattern::Pair, lorb.hpp:35-37 (16 B) */
+typedef struct lp_pair { int px, py, qx, qy; } lp_pair;
+/* Match, matchlsh.hpp:16-21 (16 B) */
+typedef struct lp_match { int query_id, train_id, distance; float quality; } lp_match;
+/* Correspondence, homography.hpp:66-70 (40 B incl. tail padding) */
+typedef struct lp_corr { double sx, sy, dx, dy; float quality; int pad_; } lp_corr;
+/* Homography, homography.hpp:17-63 (72 B) */
+typedef struct lp_homography { double h[9]; } lp_homography;
+/* Canvas, compose.hpp:18-24 (offsets omitted: not used by warp/blend) */
+typedef struct lp_canvas { int width, height, origin_x, origin_y; } lp_canvas;
+
+/* ExtractionConfig, lorb.hpp:71-90 */
+typedef struct lp_extraction_config {
+    int fast_threshold; /* uint8 range */
+    int fast_arc;
+    float harris_alpha;
+    float harris_threshold;
+    float harris_sigma;
+    int top_n;
+    int n_d;
+    float brief_blur_sigma;
+    int patch_half;
+} lp_extraction_config;
+
+/* MatchConfig, matchlsh.hpp:161-168 */
+typedef struct lp_match_config {
+    int tables, bits, t_probes, max_distance;
+    float ratio;
+    int pad_;
+    uint64_t seed;
+} lp_match_config;
+
+/* ProsacConfig, homography.hpp:156-163 (sampling: 0 = Prosac, 1 = Uniform) */
+typedef struct lp_prosac_config {
+    double threshold_px;
+    int max_iter;
+    int sampling;
+    double confidence;
+    uint64_t seed;
+    double t_total;
+} lp_prosac_config;
+
+/* StitchParams (pipeline.hpp:249-255) + CameraLayout.overlap_fraction
+ * (lorb.hpp:93-96) + PipelineConfig.homography_refresh (pipeline.hpp:199-204). */
+typedef struct lp_params {
+    lp_extraction_config extraction;
+    lp_match_config matching;
+    lp_prosac_config prosac;
+    int blend_levels;
+    int homography_refresh;
+    uint64_t seed;
+    double overlap_fraction;
+} lp_params;
+
+/* Fills the reference defaults (lorb.hpp:71-80, matchlsh.hpp:161-167,
+ * homography.hpp:156-162, pipeline.hpp:199-204,249-255, README overlap 0.25). */
+void lp_params_default(lp_params* p);
+
+/* ---- context ---- */
+typedef struct lp_ctx lp_ctx;
+lp_status lp_ctx_create(int device, lp_ctx** out);
+void lp_ctx_destroy(lp_ctx* ctx);
+/* cudaStream_t the context enqueues on (NULL = its own stream). */
+lp_status lp_ctx_set_stream(lp_ctx* ctx, void* cuda_stream);
+const char* lp_last_error(void);
+/* number of kernels this process launched through the library so far */
+uint64_t lp_kernel_launches(void);
+
+/* ---- L-ORB primitives (lorb.hpp) ---- */
+
+/* fast_corners, lorb.hpp:192-205: (x,y) pairs in raster order. */
+lp_status lp_fast_corners(lp_ctx* ctx, const uint8_t* img, int w, int h, int channels,
+                          lp_region region, int threshold, int arc, int* xy_out, int cap,
+                          int* count);
+/* harris_response, lorb.hpp:209-250 (FP64 accumulation, float result). */
+lp_status lp_harris_response(lp_ctx* ctx, const uint8_t* img, int w, int h, int channels,
+                             const int* xy, int n, float alpha, float sigma, float* out);
+/* nms, lorb.hpp:254-288: survivors in input order. */
+lp_status lp_nms(lp_ctx* ctx, const lp_keypoint* in, int n, int radius, lp_keypoint* out,
+                 int* count);
+/* select_top_n, lorb.hpp:291-299: (response desc, y asc, x asc), at most top_n. */
+lp_status lp_select_top_n(lp_ctx* ctx, const lp_keypoint* in, int n, int top_n,
+                          lp_keypoint* out, int* count);
+/* gaussian_blur, imgops.hpp:50-72 (separable, clamp-to-edge, FP32, no FMA). */
+lp_status lp_gaussian_blur(lp_ctx* ctx, const float* in, int w, int h, int channels,
+                           float sigma, float* out);
+/* brief_descriptor, lorb.hpp:333-350, batched over keypoints. */
+lp_status lp_brief_descriptors(lp_ctx* ctx, const float* smoothed, int w, int h,
+                               const lp_keypoint* kps, int n, const lp_pair* pairs, int n_d,
+                               int patch_half, uint64_t* desc_out);
+/* extract_features, lorb.hpp:388-413: all regions of one image in one pass. */
+lp_status lp_extract_features(lp_ctx* ctx, const uint8_t* img, int w, int h, int channels,
+                              const lp_region* regions, int n_regions,
+                              const lp_extraction_config* cfg, const lp_pair* pairs,
+                              lp_keypoint* kp_out, uint64_t* desc_out, int cap, int* count);
+
+/* ---- matching (matchlsh.hpp) ---- */
+
+/* descriptor_distance, matchlsh.hpp:25-33, elementwise over n pairs. */
+lp_status lp_descriptor_distances(lp_ctx* ctx, const uint64_t* a, const uint64_t* b, int n,
+                                  int n_d, int* out);
+/* match_features, matchlsh.hpp:173-193 (index on set_b, queries set_a). */
+lp_status lp_match_features(lp_ctx* ctx, const uint64_t* set_a, int na, const uint64_t* set_b,
+                            int nb, int n_d, const lp_match_config* cfg, lp_match* out, int cap,
+                            int* count);
+
+/* ---- homography (homography.hpp) ---- */
+
+/* dlt_homography, homography.hpp:114-144 */
+lp_status lp_dlt_homography(lp_ctx* ctx, const lp_corr* pairs, int n, lp_homography* out);
+/* prosac_homography, homography.hpp:182-286. trace_* optional (NULL), sized
+ * max_iter and 4*max_iter; *iterations gives the filled length. */
+lp_status lp_prosac_homography(lp_ctx* ctx, const lp_corr* matches, int n,
+                               const lp_prosac_config* cfg, lp_homography* model,
+                               uint8_t* inlier_mask, int* inlier_count, int* iterations,
+                               int* trace_pool, int* trace_samples);
+
+/* ---- compositor (compose.hpp, imgops.hpp) ---- */
+
+/* warp_image, compose.hpp:72-95 */
+lp_status lp_warp_image(lp_ctx* ctx, const float* img, int w, int h, int channels,
+                        const lp_homography* hom, const lp_canvas* canvas, float* out,
+                        float* coverage);
+/* linear_seam_mask, compose.hpp:101-131: n packed w*h coverages -> n masks */
+lp_status lp_linear_seam_mask(lp_ctx* ctx, const float* coverages, int n, int w, int h,
+                              float* masks);
+/* downsample / upsample, imgops.hpp:106-140 */
+lp_status lp_downsample(lp_ctx* ctx, const float* in, int w, int h, int channels, float* out);
+lp_status lp_upsample(lp_ctx* ctx, const float* in, int w, int h, int channels, int tw, int th,
+                      float* out);
+/* gaussian_pyramid (imgops.hpp:142-153), build_laplacian (compose.hpp:134-147):
+ * levels packed level-0 first; dims halve with floor. */
+lp_status lp_gaussian_pyramid(lp_ctx* ctx, const float* in, int w, int h, int channels,
+                              int levels, float* out_packed);
+lp_status lp_build_laplacian(lp_ctx* ctx, const float* in, int w, int h, int channels,
+                             int levels, float* out_packed);
+/* collapse_laplacian, compose.hpp:149-158 */
+lp_status lp_collapse_laplacian(lp_ctx* ctx, const float* packed, int w, int h, int channels,
+                                int levels, float* out);
+/* multiband_blend, compose.hpp:162-215: n packed images and masks */
+lp_status lp_multiband_blend(lp_ctx* ctx, const float* images, const float* masks, int n,
+                             int w, int h, int channels, int levels, uint8_t* out);
+
+/* ---- per-frame stitching engine (pipeline.hpp:419-521) ---- */
+
+typedef struct lp_rig lp_rig;
+
+/* Host-visible per-frame results (all pointers optional). Capacities are per
+ * camera (keypoints/descriptors: cap_kp) and per pair (matches: cap_matches). */
+typedef struct lp_frame_out {
+    uint8_t* panorama;        /* host or device, >= pano_cap bytes */
+    size_t pano_cap;
+    lp_canvas canvas;         /* out */
+    lp_homography* homographies; /* ncams, out (into camera-0 frame) */
+    int* kp_counts;           /* ncams */
+    lp_keypoint* keypoints;   /* ncams * cap_kp */
+    uint64_t* descriptors;    /* ncams * cap_kp * 2W */
+    int cap_kp;
+    int* match_counts;        /* ncams-1 */
+    lp_match* matches;        /* (ncams-1) * cap_matches */
+    int cap_matches;
+    int estimated;            /* out: 1 if this frame ran the estimator */
+    float stage_ms[4];        /* out: detect, describe, match_estimate, warp_blend (device time) */
+} lp_frame_out;
+
+/* StitchEngine(RigLayout{ncams identity cameras, overlap}, StitchParams, K),
+ * pipeline.hpp:343-350; all cameras w x h grayscale. */
+lp_status lp_rig_create(lp_ctx* ctx, int ncams, int w, int h, const lp_params* params,
+                        lp_rig** out);
+void lp_rig_destroy(lp_rig* rig);
+/* One frame through detect -> describe -> match_estimate (HomographyCache,
+ * pipeline.hpp:259-286) -> warp_blend. images[c] host or device. */
+lp_status lp_rig_stitch(lp_rig* rig, const uint8_t* const* images, uint64_t frame_index,
+                        lp_frame_out* out);
+/* Upper bound on panorama bytes for this rig's current homographies. */
+size_t lp_rig_panorama_capacity(lp_rig* rig);
+/* The stream the rig's work is enqueued on (cudaStream_t). */
+void* lp_rig_stream(lp_rig* rig);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif
