@@ -1443,3 +1443,86 @@ done:
     free(pano);
     return rc;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Synthetic inputs, synth.hpp:18-115 (the BASELINE configs' generators).    */
+static uint8_t to_u8_c(float v) { return to_u8(v); }
+
+int orc_synth_texture(int w, int h, uint64_t seed, float smooth_sigma, uint8_t* out) {
+    mt64 rng;
+    mt64_seed(&rng, seed);
+    const size_t n = (size_t)w * h;
+    float* noise = xcalloc(n, sizeof(float));
+    float* bl = xcalloc(n, sizeof(float));
+    for (size_t i = 0; i < n; ++i) noise[i] = (float)(mt64_next(&rng) % 256);
+    int st = orc_gaussian_blur(noise, w, h, 1, smooth_sigma, bl);
+    if (st) { free(noise); free(bl); return st; }
+    float lo = bl[0], hi = bl[0];
+    for (size_t i = 0; i < n; ++i) {
+        lo = bl[i] < lo ? bl[i] : lo; /* std::min(lo, v) */
+        hi = hi < bl[i] ? bl[i] : hi; /* std::max(hi, v) */
+    }
+    const float scale = hi > lo ? 255.0f / (hi - lo) : 0.0f;
+    for (size_t i = 0; i < n; ++i) out[i] = to_u8_c((bl[i] - lo) * scale);
+    free(noise);
+    free(bl);
+    return LP_OK;
+}
+
+int orc_synth_planted_pair(int w, int h, double overlap, uint64_t seed, uint8_t* left,
+                           uint8_t* right, double* true_h) {
+    const int shift = (int)lround(w * (1.0 - overlap));
+    const int ww = w + shift;
+    uint8_t* wide = xcalloc((size_t)ww * h, 1);
+    int st = orc_synth_texture(ww, h, seed, 1.5f, wide);
+    if (st) { free(wide); return st; }
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            left[(size_t)y * w + x] = wide[(size_t)y * ww + x];
+            right[(size_t)y * w + x] = wide[(size_t)y * ww + x + shift];
+        }
+    const double t[9] = {1, 0, (double)shift, 0, 1, 0, 0, 0, 1};
+    memcpy(true_h, t, sizeof t);
+    free(wide);
+    return LP_OK;
+}
+
+int orc_synth_sequence_frame(int w, int h, double overlap, uint64_t seed, uint64_t frame,
+                             uint8_t* left, uint8_t* right) {
+    double th[9];
+    int st = orc_synth_planted_pair(w, h, overlap, seed, left, right, th);
+    if (st) return st;
+    const int size = imax(4, h / 16);
+    const int px = (int)((frame * 7) % (uint64_t)(w - size));
+    const int py = (int)((frame * 3) % (uint64_t)(h - size));
+    for (int y = py; y < py + size; ++y)
+        for (int x = px; x < px + size; ++x) left[(size_t)y * w + x] = 255;
+    const double shift = th[2];
+    for (int y = py; y < py + size; ++y)
+        for (int x = px; x < px + size; ++x) {
+            int rx = x - (int)shift;
+            if (rx >= 0 && rx < w) right[(size_t)y * w + rx] = 255;
+        }
+    return LP_OK;
+}
+
+/* rotate, synth.hpp:37-60 */
+int orc_synth_rotate(const uint8_t* img, int w, int h, double degrees, uint8_t* out) {
+    const double rad = degrees * M_PI / 180.0;
+    const double c = cos(rad), s = sin(rad);
+    const double cx = (w - 1) / 2.0, cy = (h - 1) / 2.0;
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            double dx = x - cx, dy = y - cy;
+            double sx = c * dx + s * dy + cx;
+            double sy = -s * dx + c * dy + cy;
+            int x0 = (int)floor(sx), y0 = (int)floor(sy);
+            double ax = sx - x0, ay = sy - y0;
+#define CL(X, Y) img[(size_t)((Y) < 0 ? 0 : ((Y) >= h ? h - 1 : (Y))) * w + ((X) < 0 ? 0 : ((X) >= w ? w - 1 : (X)))]
+            double v00 = CL(x0, y0), v10 = CL(x0 + 1, y0), v01 = CL(x0, y0 + 1), v11 = CL(x0 + 1, y0 + 1);
+#undef CL
+            out[(size_t)y * w + x] =
+                to_u8_c((float)((1 - ay) * ((1 - ax) * v00 + ax * v10) + ay * ((1 - ax) * v01 + ax * v11)));
+        }
+    return LP_OK;
+}

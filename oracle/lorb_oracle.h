@@ -49,6 +49,12 @@ int orc_build_laplacian(const float* in, int w, int h, int ch, int levels, float
 int orc_collapse_laplacian(const float* packed, int w, int h, int ch, int levels, float* out);
 int orc_multiband_blend(const float* images, const float* masks, int n, int w, int h, int ch,
                         int levels, uint8_t* out);
+int orc_synth_texture(int w, int h, uint64_t seed, float smooth_sigma, uint8_t* out);
+int orc_synth_planted_pair(int w, int h, double overlap, uint64_t seed, uint8_t* left,
+                           uint8_t* right, double* true_h);
+int orc_synth_sequence_frame(int w, int h, double overlap, uint64_t seed, uint64_t frame,
+                             uint8_t* left, uint8_t* right);
+int orc_synth_rotate(const uint8_t* img, int w, int h, double degrees, uint8_t* out);
 int orc_stitch_frame(int ncams, int w, int h, const lp_params* params,
                      const uint8_t* const* images, uint64_t frame_index, lp_frame_out* out);
 

@@ -138,13 +138,13 @@ _ORACLE_EXTRA = {
     "compute_canvas": [P, P, C.c_int, C.POINTER(Canvas), P],
     "stitch_frame": [C.c_int, C.c_int, C.c_int, C.POINTER(Params), P, C.c_uint64,
                      C.POINTER(FrameOut)],
-}
-
-_REF_ONLY = {
     "synth_texture": [C.c_int, C.c_int, C.c_uint64, C.c_float, P],
     "synth_planted_pair": [C.c_int, C.c_int, C.c_double, C.c_uint64, P, P, P],
     "synth_sequence_frame": [C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_uint64, P, P],
     "synth_rotate": [P, C.c_int, C.c_int, C.c_double, P],
+}
+
+_REF_ONLY = {
     "lsh_query": [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, P, C.c_int, C.c_int, P,
                   C.c_int, c_intp],
     "run_engine": [C.c_int, C.c_int, C.c_int, C.POINTER(Params), P, C.c_int, C.c_int, C.c_int,

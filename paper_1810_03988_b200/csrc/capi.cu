@@ -1,0 +1,1005 @@
+// capi.cu — the extern "C" boundary (include/lorbpano_b200.h) and the
+// per-frame engine behind it.
+//
+// Primitives stage host pointers through stream-ordered device allocations
+// and return synchronously. The rig (lp_rig_*) is the B200 form of
+// StitchEngine's stage bodies (pipeline.hpp:419-521): all cameras' regions go
+// through one extraction launch sequence, all pairs through one matcher and
+// one PROSAC launch, and the compositor runs once per frame; device arenas are
+// sized at creation like BufferPool (pipeline.hpp:68-109) and the homography
+// cache follows HomographyCache (pipeline.hpp:259-286).
+#include <cub/cub.cuh>
+
+#include <atomic>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "compose.cuh"
+#include "homography.cuh"
+#include "host.hpp"
+#include "lorb.cuh"
+#include "match.cuh"
+
+namespace lpb {
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+static thread_local std::string g_err;
+
+template <class F>
+static lp_status guard(F&& f) {
+    try {
+        f();
+        return LP_OK;
+    } catch (const Status& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return LP_INTERNAL;
+    }
+}
+
+static bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// stream-ordered scratch buffer
+struct DBuf {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    DBuf() = default;
+    DBuf(size_t bytes, cudaStream_t st) : s(st) {
+        if (bytes) LPB_CUDA(cudaMallocAsync(&p, bytes, st));
+    }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), s(o.s) { o.p = nullptr; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            if (p) cudaFreeAsync(p, s);
+            p = o.p;
+            s = o.s;
+            o.p = nullptr;
+        }
+        return *this;
+    }
+    ~DBuf() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// device view of a caller buffer (copy-in for host memory)
+template <class T>
+struct In {
+    const T* d = nullptr;
+    std::unique_ptr<DBuf> tmp;
+    In(const T* p, size_t n, cudaStream_t s) {
+        if (!p || n == 0 || is_device_ptr(p)) {
+            d = p;
+            return;
+        }
+        tmp = std::make_unique<DBuf>(n * sizeof(T), s);
+        LPB_CUDA(cudaMemcpyAsync(tmp->p, p, n * sizeof(T), cudaMemcpyHostToDevice, s));
+        d = tmp->as<T>();
+    }
+};
+template <class T>
+struct Out {
+    T* d = nullptr;
+    T* host = nullptr;
+    size_t n = 0;
+    std::unique_ptr<DBuf> tmp;
+    Out(T* p, size_t count, cudaStream_t s) : n(count) {
+        if (!p || count == 0 || is_device_ptr(p)) {
+            d = p;
+            return;
+        }
+        host = p;
+        tmp = std::make_unique<DBuf>(count * sizeof(T), s);
+        d = tmp->as<T>();
+    }
+    void finish(cudaStream_t s, size_t count) {
+        if (host && count) LPB_CUDA(cudaMemcpyAsync(host, d, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+    }
+};
+
+template <class T>
+static DBuf upload(const std::vector<T>& v, cudaStream_t s) {
+    DBuf b(v.size() * sizeof(T), s);
+    if (!v.empty()) LPB_CUDA(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return b;
+}
+
+// status word helpers
+struct DevStatus {
+    DBuf buf;
+    explicit DevStatus(cudaStream_t s, int n = 1) : buf(sizeof(int) * n, s) {
+        LPB_CUDA(cudaMemsetAsync(buf.p, 0, sizeof(int) * n, s));
+    }
+    int* ptr() { return buf.as<int>(); }
+};
+
+static const char* status_text(int c) {
+    switch (c) {
+        case LP_WINDOW_OUT_OF_BOUNDS: return "harris_response: window does not fit";
+        case LP_PATCH_OUT_OF_BOUNDS: return "brief_descriptor: patch does not fit";
+        case LP_CAPACITY_OVERFLOW: return "device arena capacity exceeded";
+        case LP_REGION_TOO_SMALL: return "fast_corners: region too small";
+        case LP_INSUFFICIENT_MATCHES: return "need at least 4 matches";
+        case LP_NO_MODEL_FOUND: return "prosac: no hypothesis with >= 4 inliers";
+        case LP_DEGENERATE_CONFIGURATION: return "dlt: degenerate configuration";
+        case LP_NUMERICAL_FAILURE: return "dlt: h33 vanished";
+        case LP_EMPTY_INPUT: return "match_features: empty set";
+        default: return "device error";
+    }
+}
+static void sync_and_check(cudaStream_t s, int* d_status) {
+    int st = 0;
+    if (d_status) LPB_CUDA(cudaMemcpyAsync(&st, d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LPB_CUDA(cudaStreamSynchronize(s));
+    if (st) throw Status(static_cast<lp_status>(st), status_text(st));
+}
+
+static void validate_ext(const lp_extraction_config& c) {  // lorb.hpp:82-89
+    if (c.fast_arc < 9 || c.fast_arc > 16) throw Status(LP_BAD_PARAMS, "fast_arc must be in [9,16]");
+    if (c.top_n < 4) throw Status(LP_BAD_PARAMS, "top_n must be >= 4");
+    if (c.n_d < 64 || c.n_d > 512) throw Status(LP_BAD_PARAMS, "n_d must be in [64,512]");
+    if (!(c.harris_sigma > 0.0f)) throw Status(LP_INVALID_SIGMA, "harris_sigma must be > 0");
+    if (!(c.brief_blur_sigma > 0.0f)) throw Status(LP_INVALID_SIGMA, "brief_blur_sigma must be > 0");
+    if (c.patch_half < 1) throw Status(LP_BAD_PARAMS, "patch_half must be >= 1");
+    if (c.top_n > kTopnSortCap) throw Status(LP_BAD_PARAMS, "top_n above the device sort capacity");
+}
+
+// Constant per-configuration tables for the extractor.
+struct ExtractTables {
+    DBuf harris_w, taps, pairs;
+    int harris_r = 0, blur_r = 0;
+    ExtractTables(const lp_extraction_config& c, const std::vector<lp_pair>& pat, cudaStream_t s) {
+        auto hw = host::harris_weights(c.harris_sigma, &harris_r);
+        if (harris_r > kMaxHarrisR) throw Status(LP_BAD_PARAMS, "harris_sigma too large for the device tile");
+        auto tp = host::gaussian_kernel(c.brief_blur_sigma);
+        blur_r = static_cast<int>(tp.size() / 2);
+        if (blur_r > kMaxBlurR) throw Status(LP_BAD_PARAMS, "brief_blur_sigma too large");
+        harris_w = upload(hw, s);
+        taps = upload(tp, s);
+        pairs = upload(pat, s);
+    }
+};
+
+// Build DevRegions (scan areas + tiles) for regions over a set of images.
+static std::vector<DevRegion> make_dev_regions(const std::vector<lp_region>& regs,
+                                               const std::vector<int>& img_of,
+                                               const std::vector<int>& slot_of, const int* w,
+                                               const int* h, int* total_tiles) {
+    std::vector<DevRegion> out;
+    int base = 0;
+    for (size_t i = 0; i < regs.size(); ++i) {
+        const lp_region& r = regs[i];
+        const int im = img_of[i];
+        DevRegion d;
+        d.img = im;
+        d.x0 = std::max(r.x0, 3);
+        d.x1 = std::min(r.x1, w[im] - 3);
+        d.y0 = std::max(r.y0, 3);
+        d.y1 = std::min(r.y1, h[im] - 3);
+        if (d.x0 >= d.x1 || d.y0 >= d.y1) throw Status(LP_REGION_TOO_SMALL, "fast_corners: region too small");
+        if (w[im] > 65535 || h[im] > 65535) throw Status(LP_BAD_PARAMS, "image dimension above 65535");
+        d.rx0 = r.x0;
+        d.ry0 = r.y0;
+        d.rx1 = r.x1;
+        d.ry1 = r.y1;
+        d.tiles_x = cdiv(d.x1 - d.x0, kDetTile);
+        d.tile_base = base;
+        d.out_slot = slot_of[i];
+        base += d.tiles_x * cdiv(d.y1 - d.y0, kDetTile);
+        out.push_back(d);
+    }
+    *total_tiles = base;
+    return out;
+}
+
+static size_t surv_cap_for(const DevRegion& d) {
+    return static_cast<size_t>((d.x1 - d.x0 + 1) / 2) * ((d.y1 - d.y0 + 1) / 2) + 64;
+}
+
+}  // namespace lpb
+
+using namespace lpb;
+
+struct lp_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+};
+
+extern "C" {
+
+const char* lp_last_error(void) { return g_err.c_str(); }
+uint64_t lp_kernel_launches(void) { return g_launches.load(); }
+
+void lp_params_default(lp_params* p) {
+    std::memset(p, 0, sizeof *p);
+    p->extraction = lp_extraction_config{20, 9, 0.04f, 0.0f, 1.0f, 500, 256, 2.0f, 15};
+    p->matching.tables = 4;
+    p->matching.bits = 16;
+    p->matching.t_probes = 16;
+    p->matching.max_distance = 64;
+    p->matching.ratio = 0.8f;
+    p->matching.seed = 0;
+    p->prosac.threshold_px = 3.0;
+    p->prosac.max_iter = 1000;
+    p->prosac.sampling = 0;
+    p->prosac.confidence = 0.99;
+    p->prosac.seed = 0;
+    p->prosac.t_total = 200000.0;
+    p->blend_levels = 4;
+    p->homography_refresh = 1;
+    p->seed = 0;
+    p->overlap_fraction = 0.25;
+}
+
+lp_status lp_ctx_create(int device, lp_ctx** out) {
+    return guard([&] {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            throw Status(LP_NO_DEVICE, "no CUDA device");
+        }
+        LPB_CUDA(cudaSetDevice(device));
+        auto* c = new lp_ctx;
+        c->device = device;
+        LPB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+        *out = c;
+    });
+}
+void lp_ctx_destroy(lp_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+lp_status lp_ctx_set_stream(lp_ctx* ctx, void* s) {
+    return guard([&] {
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        ctx->own_stream = false;
+        ctx->stream = static_cast<cudaStream_t>(s);
+    });
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_iota(int* p, int n) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = i;
+}
+__global__ void k_xy_from_index(const int* idx, int n, int x0, int sw, int y0, int* xy) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    xy[2 * i] = x0 + idx[i] % sw;
+    xy[2 * i + 1] = y0 + idx[i] / sw;
+}
+
+lp_status lp_fast_corners(lp_ctx* ctx, const uint8_t* img, int w, int h, int ch, lp_region r,
+                          int thr, int arc, int* xy_out, int cap, int* count) {
+    return guard([&] {
+        if (ch != 1) throw Status(LP_UNSUPPORTED_FORMAT, "fast_corners: grayscale input required");
+        const int x0 = std::max(r.x0, 3), x1 = std::min(r.x1, w - 3);
+        const int y0 = std::max(r.y0, 3), y1 = std::min(r.y1, h - 3);
+        if (x0 >= x1 || y0 >= y1) throw Status(LP_REGION_TOO_SMALL, "fast_corners: region too small");
+        cudaStream_t s = ctx->stream;
+        In<uint8_t> dimg(img, static_cast<size_t>(w) * h, s);
+        const int sw = x1 - x0;
+        const int n = sw * (y1 - y0);
+        DBuf flags(n, s), idx(sizeof(int) * n, s), nsel(sizeof(int), s), lin(sizeof(int) * n, s);
+        fast_flags_launch(dimg.d, w, h, x0, y0, x1, y1, static_cast<uint8_t>(thr), arc, flags.as<uint8_t>(), s);
+        LPB_LAUNCH(k_iota, cdiv(n, 256), 256, 0, s, lin.as<int>(), n);
+        size_t tb = 0;
+        const int* it = lin.as<int>();
+        cub::DeviceSelect::Flagged(nullptr, tb, it, flags.as<uint8_t>(), idx.as<int>(), nsel.as<int>(), n, s);
+        DBuf tmp(tb, s);
+        cub::DeviceSelect::Flagged(tmp.p, tb, it, flags.as<uint8_t>(), idx.as<int>(), nsel.as<int>(), n, s);
+        int total = 0;
+        LPB_CUDA(cudaMemcpyAsync(&total, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        LPB_CUDA(cudaStreamSynchronize(s));
+        const int k = std::min(total, cap);
+        Out<int> dxy(xy_out, static_cast<size_t>(2) * k, s);
+        if (k > 0) {
+            LPB_LAUNCH(k_xy_from_index, cdiv(k, 256), 256, 0, s, idx.as<int>(), k, x0, sw, y0, dxy.d);
+            dxy.finish(s, static_cast<size_t>(2) * k);
+        }
+        LPB_CUDA(cudaStreamSynchronize(s));
+        *count = total;
+    });
+}
+
+lp_status lp_harris_response(lp_ctx* ctx, const uint8_t* img, int w, int h, int ch, const int* xy,
+                             int n, float alpha, float sigma, float* out) {
+    return guard([&] {
+        if (ch != 1) throw Status(LP_UNSUPPORTED_FORMAT, "harris_response: grayscale input required");
+        if (n == 0) return;
+        cudaStream_t s = ctx->stream;
+        int r = 0;
+        auto wts = host::harris_weights(sigma, &r);
+        DBuf dw = upload(wts, s);
+        In<uint8_t> dimg(img, static_cast<size_t>(w) * h, s);
+        In<int> dxy(xy, static_cast<size_t>(2) * n, s);
+        Out<float> dout(out, n, s);
+        DevStatus st(s);
+        harris_points_launch(dimg.d, w, h, dxy.d, n, dw.as<double>(), r, alpha, dout.d, st.ptr(), s);
+        sync_and_check(s, st.ptr());
+        dout.finish(s, n);
+        LPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+lp_status lp_nms(lp_ctx* ctx, const lp_keypoint* in, int n, int radius, lp_keypoint* out, int* count) {
+    return guard([&] {
+        *count = 0;
+        if (n == 0) return;
+        cudaStream_t s = ctx->stream;
+        std::vector<lp_keypoint> hk(n);
+        if (is_device_ptr(in)) {
+            LPB_CUDA(cudaMemcpyAsync(hk.data(), in, sizeof(lp_keypoint) * n, cudaMemcpyDeviceToHost, s));
+            LPB_CUDA(cudaStreamSynchronize(s));
+        } else {
+            std::memcpy(hk.data(), in, sizeof(lp_keypoint) * n);
+        }
+        int minx = hk[0].x, maxx = hk[0].x, miny = hk[0].y, maxy = hk[0].y;
+        for (auto& k : hk) {
+            minx = std::min(minx, k.x);
+            maxx = std::max(maxx, k.x);
+            miny = std::min(miny, k.y);
+            maxy = std::max(maxy, k.y);
+        }
+        const int gw = maxx - minx + 1, gh = maxy - miny + 1;
+        DBuf dk = upload(hk, s);
+        DBuf grid(sizeof(int) * static_cast<size_t>(gw) * gh, s), keep(n, s), sel(sizeof(lp_keypoint) * n, s),
+            nsel(sizeof(int), s);
+        nms_generic_launch(dk.as<lp_keypoint>(), n, radius, minx, miny, gw, gh, grid.as<int>(), keep.as<uint8_t>(), s);
+        size_t tb = 0;
+        cub::DeviceSelect::Flagged(nullptr, tb, dk.as<lp_keypoint>(), keep.as<uint8_t>(), sel.as<lp_keypoint>(),
+                                   nsel.as<int>(), n, s);
+        DBuf tmp(tb, s);
+        cub::DeviceSelect::Flagged(tmp.p, tb, dk.as<lp_keypoint>(), keep.as<uint8_t>(), sel.as<lp_keypoint>(),
+                                   nsel.as<int>(), n, s);
+        int k = 0;
+        LPB_CUDA(cudaMemcpyAsync(&k, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        LPB_CUDA(cudaStreamSynchronize(s));
+        if (is_device_ptr(out))
+            LPB_CUDA(cudaMemcpyAsync(out, sel.p, sizeof(lp_keypoint) * k, cudaMemcpyDeviceToDevice, s));
+        else
+            LPB_CUDA(cudaMemcpyAsync(out, sel.p, sizeof(lp_keypoint) * k, cudaMemcpyDeviceToHost, s));
+        LPB_CUDA(cudaStreamSynchronize(s));
+        *count = k;
+    });
+}
+
+__global__ void k_sort_key(const lp_keypoint* kp, const int* idx, int n, int field, uint32_t* key) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const lp_keypoint k = kp[idx[i]];
+    key[i] = field == 0 ? (static_cast<uint32_t>(k.x) ^ 0x80000000u)
+                        : field == 1 ? (static_cast<uint32_t>(k.y) ^ 0x80000000u) : float_key(k.response);
+}
+__global__ void k_gather_kp(const lp_keypoint* kp, const int* idx, int n, lp_keypoint* out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = kp[idx[i]];
+}
+
+lp_status lp_select_top_n(lp_ctx* ctx, const lp_keypoint* in, int n, int top_n, lp_keypoint* out,
+                          int* count) {
+    return guard([&] {
+        if (top_n < 1) throw Status(LP_BAD_PARAMS, "select_top_n: n must be >= 1");
+        *count = 0;
+        if (n == 0) return;
+        cudaStream_t s = ctx->stream;
+        In<lp_keypoint> dk(in, n, s);
+        DBuf ia(sizeof(int) * n, s), ib(sizeof(int) * n, s), ka(sizeof(uint32_t) * n, s), kb(sizeof(uint32_t) * n, s);
+        LPB_LAUNCH(k_iota, cdiv(n, 256), 256, 0, s, ia.as<int>(), n);
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, ka.as<uint32_t>(), kb.as<uint32_t>(), ia.as<int>(), ib.as<int>(), n,
+                                        0, 32, s);
+        DBuf tmp(tb, s);
+        // stable LSD passes: x asc, then y asc, then response desc (lorb.hpp:293-296)
+        for (int field = 0; field < 3; ++field) {
+            LPB_LAUNCH(k_sort_key, cdiv(n, 256), 256, 0, s, dk.d, ia.as<int>(), n, field, ka.as<uint32_t>());
+            if (field < 2)
+                cub::DeviceRadixSort::SortPairs(tmp.p, tb, ka.as<uint32_t>(), kb.as<uint32_t>(), ia.as<int>(),
+                                                ib.as<int>(), n, 0, 32, s);
+            else
+                cub::DeviceRadixSort::SortPairsDescending(tmp.p, tb, ka.as<uint32_t>(), kb.as<uint32_t>(),
+                                                          ia.as<int>(), ib.as<int>(), n, 0, 32, s);
+            LPB_CUDA(cudaMemcpyAsync(ia.p, ib.p, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+        }
+        const int k = std::min(n, top_n);
+        Out<lp_keypoint> dout(out, k, s);
+        LPB_LAUNCH(k_gather_kp, cdiv(k, 256), 256, 0, s, dk.d, ia.as<int>(), k, dout.d);
+        dout.finish(s, k);
+        LPB_CUDA(cudaStreamSynchronize(s));
+        *count = k;
+    });
+}
+
+lp_status lp_gaussian_blur(lp_ctx* ctx, const float* in, int w, int h, int ch, float sigma, float* out) {
+    return guard([&] {
+        auto taps = host::gaussian_kernel(sigma);
+        cudaStream_t s = ctx->stream;
+        const size_t n = static_cast<size_t>(w) * h * ch;
+        DBuf dt = upload(taps, s), tmp(sizeof(float) * n, s);
+        In<float> di(in, n, s);
+        Out<float> dout(out, n, s);
+        blur_launch(di.d, tmp.as<float>(), dout.d, w, h, ch, dt.as<float>(), static_cast<int>(taps.size() / 2), s);
+        dout.finish(s, n);
+        LPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+lp_status lp_brief_descriptors(lp_ctx* ctx, const float* sm, int w, int h, const lp_keypoint* kps, int n,
+                               const lp_pair* pairs, int n_d, int ph, uint64_t* out) {
+    return guard([&] {
+        if (n == 0) return;
+        cudaStream_t s = ctx->stream;
+        const int W2 = 2 * ((n_d + 63) / 64);
+        In<float> dsm(sm, static_cast<size_t>(w) * h, s);
+        In<lp_keypoint> dk(kps, n, s);
+        In<lp_pair> dp(pairs, n_d, s);
+        Out<uint64_t> dout(out, static_cast<size_t>(n) * W2, s);
+        DevStatus st(s);
+        brief_generic_launch(dsm.d, w, h, dk.d, n, dp.d, n_d, ph, dout.d, st.ptr(), s);
+        sync_and_check(s, st.ptr());
+        dout.finish(s, static_cast<size_t>(n) * W2);
+        LPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+lp_status lp_extract_features(lp_ctx* ctx, const uint8_t* img, int w, int h, int ch,
+                              const lp_region* regions, int nreg, const lp_extraction_config* cfg,
+                              const lp_pair* pairs, lp_keypoint* kp_out, uint64_t* desc_out, int cap,
+                              int* count) {
+    return guard([&] {
+        validate_ext(*cfg);
+        if (ch != 1) throw Status(LP_UNSUPPORTED_FORMAT, "fast_corners: grayscale input required");
+        *count = 0;
+        if (nreg == 0) return;
+        cudaStream_t s = ctx->stream;
+        std::vector<lp_region> regs(regions, regions + nreg);
+        std::vector<lp_pair> pat(pairs, pairs + cfg->n_d);
+        std::vector<int> zeros(nreg, 0);
+        int tiles = 0;
+        auto dregs = make_dev_regions(regs, zeros, zeros, &w, &h, &tiles);
+        size_t scap = 0;
+        for (auto& d : dregs) scap = std::max(scap, surv_cap_for(d));
+        ExtractTables T(*cfg, pat, s);
+        In<uint8_t> dimg(img, static_cast<size_t>(w) * h, s);
+        std::vector<DevImage> ims{DevImage{dimg.d, w, h}};
+        DBuf dims = upload(ims, s), dr = upload(dregs, s);
+        const int W2 = 2 * ((cfg->n_d + 63) / 64);
+        const int cap_slot = nreg * cfg->top_n;
+        DBuf surv(sizeof(uint64_t) * scap * nreg, s), scount(sizeof(unsigned) * nreg, s),
+            kpr(sizeof(lp_keypoint) * static_cast<size_t>(nreg) * cfg->top_n, s), cr(sizeof(int) * nreg, s),
+            kpo(sizeof(lp_keypoint) * cap_slot, s), dso(sizeof(uint64_t) * static_cast<size_t>(cap_slot) * W2, s),
+            sc(sizeof(int), s);
+        DevStatus st(s);
+        ExtractArgs a{};
+        a.regions = dr.as<DevRegion>();
+        a.nregions = nreg;
+        a.total_tiles = tiles;
+        a.images = dims.as<DevImage>();
+        a.harris_w = T.harris_w.as<double>();
+        a.harris_r = T.harris_r;
+        a.alpha = cfg->harris_alpha;
+        a.threshold = cfg->harris_threshold;
+        a.fast_t = static_cast<uint8_t>(cfg->fast_threshold);
+        a.fast_arc = cfg->fast_arc;
+        a.top_n = cfg->top_n;
+        a.surv = surv.as<uint64_t>();
+        a.surv_count = scount.as<unsigned>();
+        a.surv_cap = static_cast<int>(scap);
+        a.kp_region = kpr.as<lp_keypoint>();
+        a.count_region = cr.as<int>();
+        a.blur_taps = T.taps.as<float>();
+        a.blur_r = T.blur_r;
+        a.pairs = T.pairs.as<lp_pair>();
+        a.n_d = cfg->n_d;
+        a.patch_half = cfg->patch_half;
+        a.nslots = 1;
+        a.kp_out = kpo.as<lp_keypoint>();
+        a.desc_out = dso.as<uint64_t>();
+        a.cap_slot = cap_slot;
+        a.slot_count = sc.as<int>();
+        a.status = st.ptr();
+        extract_launch(a, s);
+        sync_and_check(s, st.ptr());
+        int total = 0;
+        LPB_CUDA(cudaMemcpy(&total, sc.p, sizeof(int), cudaMemcpyDeviceToHost));
+        const int k = std::min(total, cap);
+        auto kind_k = is_device_ptr(kp_out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        auto kind_d = is_device_ptr(desc_out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        if (k > 0) {
+            LPB_CUDA(cudaMemcpyAsync(kp_out, kpo.p, sizeof(lp_keypoint) * k, kind_k, s));
+            LPB_CUDA(cudaMemcpyAsync(desc_out, dso.p, sizeof(uint64_t) * k * W2, kind_d, s));
+        }
+        LPB_CUDA(cudaStreamSynchronize(s));
+        *count = total;
+    });
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_distances(const uint64_t* a, const uint64_t* b, int n, int W2, int* out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int d = 0;
+    for (int w = 0; w < W2; ++w) d += __popcll(a[static_cast<size_t>(i) * W2 + w] ^ b[static_cast<size_t>(i) * W2 + w]);
+    out[i] = d;
+}
+lp_status lp_descriptor_distances(lp_ctx* ctx, const uint64_t* a, const uint64_t* b, int n, int n_d, int* out) {
+    return guard([&] {
+        if (n == 0) return;
+        cudaStream_t s = ctx->stream;
+        const int W2 = 2 * ((n_d + 63) / 64);
+        In<uint64_t> da(a, static_cast<size_t>(n) * W2, s), db(b, static_cast<size_t>(n) * W2, s);
+        Out<int> dout(out, n, s);
+        LPB_LAUNCH(k_distances, cdiv(n, 256), 256, 0, s, da.d, db.d, n, W2, dout.d);
+        dout.finish(s, n);
+        LPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+// constant matcher tables
+struct MatchTables {
+    DBuf bitpos, partial;
+    host::ProbeSet ps;
+    MatchTables(int n_d, const lp_match_config& c, cudaStream_t s) {
+        auto bp = host::lsh_bit_positions(n_d, c.tables, c.bits, c.seed);
+        ps = host::probe_set(c.bits, c.t_probes);
+        bitpos = upload(bp, s);
+        partial = upload(ps.partial, s);
+    }
+    void fill(MatchArgs& a, const lp_match_config& c) const {
+        a.bitpos = bitpos.as<int>();
+        a.tables = c.tables;
+        a.bits = c.bits;
+        a.full_card = ps.full_card;
+        a.partial = partial.as<uint64_t>();
+        a.npartial = static_cast<int>(ps.partial.size());
+        a.max_distance = c.max_distance;
+        a.ratio = c.ratio;
+    }
+};
+
+lp_status lp_match_features(lp_ctx* ctx, const uint64_t* set_a, int na, const uint64_t* set_b, int nb,
+                            int n_d, const lp_match_config* cfg, lp_match* out, int cap, int* count) {
+    return guard([&] {
+        if (na == 0 || nb == 0) throw Status(LP_EMPTY_INPUT, "match_features: empty set");
+        cudaStream_t s = ctx->stream;
+        MatchTables T(n_d, *cfg, s);
+        const int W2 = 2 * ((n_d + 63) / 64);
+        const int capn = std::max(na, nb);
+        DBuf desc(sizeof(uint64_t) * 2 * capn * W2, s), kps(sizeof(lp_keypoint) * 2 * capn, s),
+            counts(sizeof(int) * 2, s), keys(sizeof(uint64_t) * 2 * capn * cfg->tables, s),
+            qres(sizeof(int4) * capn, s), matches(sizeof(lp_match) * capn, s), corr(sizeof(lp_corr) * capn, s),
+            mc(sizeof(int), s);
+        DevStatus pst(s);
+        auto kind = [](const void* p) { return is_device_ptr(p) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice; };
+        LPB_CUDA(cudaMemcpyAsync(desc.p, set_b, sizeof(uint64_t) * nb * W2, kind(set_b), s));
+        LPB_CUDA(cudaMemcpyAsync(desc.as<uint64_t>() + static_cast<size_t>(capn) * W2, set_a,
+                                 sizeof(uint64_t) * na * W2, kind(set_a), s));
+        LPB_CUDA(cudaMemsetAsync(kps.p, 0, sizeof(lp_keypoint) * 2 * capn, s));
+        int hc[2] = {nb, na};
+        LPB_CUDA(cudaMemcpyAsync(counts.p, hc, sizeof hc, cudaMemcpyHostToDevice, s));
+        MatchArgs a{};
+        a.npairs = 1;
+        a.qslot0 = 1;
+        a.tslot0 = 0;
+        a.nslots = 2;
+        a.desc = desc.as<uint64_t>();
+        a.kps = kps.as<lp_keypoint>();
+        a.counts = counts.as<int>();
+        a.cap = capn;
+        a.n_d = n_d;
+        T.fill(a, *cfg);
+        a.keys = keys.as<uint64_t>();
+        a.qres = qres.as<int4>();
+        a.matches = matches.as<lp_match>();
+        a.corr = corr.as<lp_corr>();
+        a.match_counts = mc.as<int>();
+        a.pair_status = pst.ptr();
+        match_launch(a, s);
+        sync_and_check(s, pst.ptr());
+        int n = 0;
+        LPB_CUDA(cudaMemcpy(&n, mc.p, sizeof(int), cudaMemcpyDeviceToHost));
+        const int k = std::min(n, cap);
+        if (k > 0)
+            LPB_CUDA(cudaMemcpyAsync(out, matches.p, sizeof(lp_match) * k,
+                                     is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+        LPB_CUDA(cudaStreamSynchronize(s));
+        *count = n;
+    });
+}
+
+// ---------------------------------------------------------------------------
+lp_status lp_dlt_homography(lp_ctx* ctx, const lp_corr* pairs, int n, lp_homography* out) {
+    return guard([&] {
+        if (n < 4) throw Status(LP_INSUFFICIENT_MATCHES, "dlt: need at least 4 pairs");
+        cudaStream_t s = ctx->stream;
+        In<lp_corr> dc(pairs, n, s);
+        DBuf scratch(sizeof(double) * (static_cast<size_t>(2 * n) * 9 + 2 * n + n), s), dh(sizeof(lp_homography), s);
+        DevStatus st(s);
+        dlt_launch(dc.d, n, scratch.as<double>(), dh.as<lp_homography>(), st.ptr(), s);
+        sync_and_check(s, st.ptr());
+        LPB_CUDA(cudaMemcpy(out, dh.p, sizeof(lp_homography), cudaMemcpyDeviceToHost));
+    });
+}
+
+lp_status lp_prosac_homography(lp_ctx* ctx, const lp_corr* matches, int n, const lp_prosac_config* cfg,
+                               lp_homography* model, uint8_t* mask, int* inlier_count, int* iterations,
+                               int* trace_pool, int* trace_samples) {
+    return guard([&] {
+        *iterations = 0;
+        if (n < 4) throw Status(LP_INSUFFICIENT_MATCHES, "prosac: need at least 4 matches");
+        cudaStream_t s = ctx->stream;
+        // termination table row for this n (host glibc, exact)
+        std::vector<int> row(static_cast<size_t>(n) + 1, cfg->max_iter + 1);
+        {
+            auto tab = host::prosac_exit_table(n, cfg->max_iter, cfg->confidence);
+            for (int c = 0; c <= n; ++c) row[c] = tab[static_cast<size_t>(n) * (n + 1) + c];
+        }
+        In<lp_corr> dc(matches, n, s);
+        const int mi = std::max(cfg->max_iter, 1);
+        DBuf drow = upload(row, s), cnt(sizeof(int), s), scratch(sizeof(double) * (static_cast<size_t>(2 * n) * 9 + 3 * n), s),
+            dm(sizeof(lp_homography), s), dmask(n, s), dic(sizeof(int), s), dit(sizeof(int), s),
+            tp(sizeof(int) * mi, s), ts(sizeof(int) * mi * 4, s);
+        DevStatus pst(s);
+        LPB_CUDA(cudaMemcpyAsync(cnt.p, &n, sizeof(int), cudaMemcpyHostToDevice, s));
+        ProsacArgs a{};
+        a.npairs = 1;
+        a.corr = dc.d;
+        a.counts = cnt.as<int>();
+        a.cap = n;
+        a.threshold = cfg->threshold_px;
+        a.max_iter = cfg->max_iter;
+        a.uniform = cfg->sampling;
+        a.t_total = cfg->t_total;
+        a.seed = cfg->seed;
+        a.frame = 0;
+        a.per_pair_seed = 0;
+        a.exit_tab = drow.as<int>();
+        a.nmax = 0;
+        a.scratch = scratch.as<double>();
+        a.model = dm.as<lp_homography>();
+        a.mask = dmask.as<uint8_t>();
+        a.inlier_count = dic.as<int>();
+        a.iterations = dit.as<int>();
+        a.trace_pool = tp.as<int>();
+        a.trace_samples = ts.as<int>();
+        a.pair_status = pst.ptr();
+        prosac_launch(a, s);
+        int st = 0, its = 0;
+        LPB_CUDA(cudaMemcpyAsync(&st, pst.ptr(), sizeof(int), cudaMemcpyDeviceToHost, s));
+        LPB_CUDA(cudaMemcpyAsync(&its, dit.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        LPB_CUDA(cudaStreamSynchronize(s));
+        *iterations = its;
+        if (trace_pool && its > 0) LPB_CUDA(cudaMemcpy(trace_pool, tp.p, sizeof(int) * its, cudaMemcpyDeviceToHost));
+        if (trace_samples && its > 0)
+            LPB_CUDA(cudaMemcpy(trace_samples, ts.p, sizeof(int) * its * 4, cudaMemcpyDeviceToHost));
+        if (st) throw Status(static_cast<lp_status>(st), status_text(st));
+        LPB_CUDA(cudaMemcpy(model, dm.p, sizeof(lp_homography), cudaMemcpyDeviceToHost));
+        if (mask) LPB_CUDA(cudaMemcpy(mask, dmask.p, n, is_device_ptr(mask) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+        LPB_CUDA(cudaMemcpy(inlier_count, dic.p, sizeof(int), cudaMemcpyDeviceToHost));
+    });
+}
+
+// ---------------------------------------------------------------------------
+lp_status lp_warp_image(lp_ctx* ctx, const float* img, int w, int h, int ch, const lp_homography* hom,
+                        const lp_canvas* cv, float* out, float* coverage) {
+    return guard([&] {
+        if (std::abs(host::h_det(hom->h)) < 1e-9) throw Status(LP_SINGULAR_HOMOGRAPHY, "warp_image: singular homography");
+        double hi[9];
+        host::h_inverse(hom->h, hi);
+        cudaStream_t s = ctx->stream;
+        std::vector<double> hv(hi, hi + 9);
+        DBuf dh = upload(hv, s);
+        const size_t np = static_cast<size_t>(cv->width) * cv->height;
+        In<float> di(img, static_cast<size_t>(w) * h * ch, s);
+        Out<float> dout(out, np * ch, s), dcov(coverage, np, s);
+        warp_generic_launch(di.d, w, h, ch, dh.as<double>(), cv->width, cv->height, cv->origin_x, cv->origin_y,
+                            dout.d, dcov.d, s);
+        dout.finish(s, np * ch);
+        dcov.finish(s, np);
+        LPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+lp_status lp_linear_seam_mask(lp_ctx* ctx, const float* covs, int n, int w, int h, float* masks) {
+    return guard([&] {
+        if (n < 1) throw Status(LP_BAD_PARAMS, "linear_seam_mask: no coverage masks");
+        cudaStream_t s = ctx->stream;
+        const size_t np = static_cast<size_t>(w) * h * n;
+        In<float> dc(covs, np, s);
+        Out<float> dm(masks, np, s);
+        seam_generic_launch(dc.d, n, w, h, dm.d, s);
+        dm.finish(s, np);
+        LPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+lp_status lp_downsample(lp_ctx* ctx, const float* in, int w, int h, int ch, float* out) {
+    return guard([&] {
+        if (w < 2 || h < 2) throw Status(LP_IMAGE_TOO_SMALL, "downsample: need at least 2x2");
+        cudaStream_t s = ctx->stream;
+        DBuf taps = upload(host::gaussian_kernel(1.0f), s), tmp(sizeof(float) * (w / 2) * h * ch, s);
+        In<float> di(in, static_cast<size_t>(w) * h * ch, s);
+        const size_t no = static_cast<size_t>(w / 2) * (h / 2) * ch;
+        Out<float> dout(out, no, s);
+        downsample_launch(di.d, w, h, ch, taps.as<float>(), tmp.as<float>(), dout.d, s);
+        dout.finish(s, no);
+        LPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+lp_status lp_upsample(lp_ctx* ctx, const float* in, int w, int h, int ch, int tw, int th, float* out) {
+    return guard([&] {
+        if (std::abs(tw - 2 * w) > 1 || std::abs(th - 2 * h) > 1)
+            throw Status(LP_BAD_TARGET_DIMS, "upsample: target dims must be ~2x source");
+        cudaStream_t s = ctx->stream;
+        In<float> di(in, static_cast<size_t>(w) * h * ch, s);
+        const size_t no = static_cast<size_t>(tw) * th * ch;
+        Out<float> dout(out, no, s);
+        upsample_launch(di.d, w, h, ch, tw, th, dout.d, s);
+        dout.finish(s, no);
+        LPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+static size_t pyr_total(int w, int h, int ch, int levels) {
+    size_t t = 0;
+    for (int k = 0; k < levels; ++k) {
+        t += static_cast<size_t>(w) * h * ch;
+        w /= 2;
+        h /= 2;
+    }
+    return t;
+}
+
+// gaussian_pyramid into a packed device buffer (imgops.hpp:142-153)
+static void pyramid_dev(const float* in, int w, int h, int ch, int levels, float* out, cudaStream_t s) {
+    if (levels < 1) throw Status(LP_TOO_MANY_LEVELS, "pyramid: levels must be >= 1");
+    {
+        int lw = w, lh = h;
+        for (int i = 1; i < levels; ++i) {
+            if (lw < 2 || lh < 2) throw Status(LP_TOO_MANY_LEVELS, "pyramid: image too small for requested levels");
+            lw /= 2;
+            lh /= 2;
+        }
+    }
+    LPB_CUDA(cudaMemcpyAsync(out, in, sizeof(float) * w * h * ch, cudaMemcpyDeviceToDevice, s));
+    DBuf taps = upload(host::gaussian_kernel(1.0f), s), tmp(sizeof(float) * std::max(1, w / 2) * h * ch, s);
+    float* prev = out;
+    for (int i = 1; i < levels; ++i) {
+        float* next = prev + static_cast<size_t>(w) * h * ch;
+        downsample_launch(prev, w, h, ch, taps.as<float>(), tmp.as<float>(), next, s);
+        prev = next;
+        w /= 2;
+        h /= 2;
+    }
+}
+
+lp_status lp_gaussian_pyramid(lp_ctx* ctx, const float* in, int w, int h, int ch, int levels, float* out) {
+    return guard([&] {
+        cudaStream_t s = ctx->stream;
+        if (levels < 1) throw Status(LP_TOO_MANY_LEVELS, "pyramid: levels must be >= 1");
+        const size_t tot = pyr_total(w, h, ch, levels);
+        In<float> di(in, static_cast<size_t>(w) * h * ch, s);
+        Out<float> dout(out, tot, s);
+        pyramid_dev(di.d, w, h, ch, levels, dout.d, s);
+        dout.finish(s, tot);
+        LPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+lp_status lp_build_laplacian(lp_ctx* ctx, const float* in, int w, int h, int ch, int levels, float* out) {
+    return guard([&] {
+        cudaStream_t s = ctx->stream;
+        if (levels < 1) throw Status(LP_TOO_MANY_LEVELS, "build_laplacian: levels must be >= 1");
+        const size_t tot = pyr_total(w, h, ch, levels);
+        In<float> di(in, static_cast<size_t>(w) * h * ch, s);
+        Out<float> dout(out, tot, s);
+        pyramid_dev(di.d, w, h, ch, levels, dout.d, s);
+        DBuf up(sizeof(float) * static_cast<size_t>(w) * h * ch, s);
+        float* lv = dout.d;
+        int lw = w, lh = h;
+        for (int k = 0; k + 1 < levels; ++k) {
+            float* nx = lv + static_cast<size_t>(lw) * lh * ch;
+            upsample_launch(nx, lw / 2, lh / 2, ch, lw, lh, up.as<float>(), s);
+            sub_launch(lv, up.as<float>(), static_cast<size_t>(lw) * lh * ch, s);
+            lv = nx;
+            lw /= 2;
+            lh /= 2;
+        }
+        dout.finish(s, tot);
+        LPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+lp_status lp_collapse_laplacian(lp_ctx* ctx, const float* packed, int w, int h, int ch, int levels, float* out) {
+    return guard([&] {
+        if (levels < 1) throw Status(LP_TOO_MANY_LEVELS, "collapse_laplacian: empty pyramid");
+        cudaStream_t s = ctx->stream;
+        const size_t tot = pyr_total(w, h, ch, levels);
+        In<float> dp(packed, tot, s);
+        std::vector<const float*> lv(levels);
+        std::vector<int> dw(levels), dh(levels);
+        const float* p = dp.d;
+        int lw = w, lh = h;
+        for (int k = 0; k < levels; ++k) {
+            lv[k] = p;
+            dw[k] = lw;
+            dh[k] = lh;
+            p += static_cast<size_t>(lw) * lh * ch;
+            lw /= 2;
+            lh /= 2;
+        }
+        DBuf a(sizeof(float) * static_cast<size_t>(w) * h * ch, s), b(sizeof(float) * static_cast<size_t>(w) * h * ch, s);
+        float* acc = a.as<float>();
+        float* nxt = b.as<float>();
+        const size_t ntop = static_cast<size_t>(dw[levels - 1]) * dh[levels - 1] * ch;
+        LPB_CUDA(cudaMemcpyAsync(acc, lv[levels - 1], sizeof(float) * ntop, cudaMemcpyDeviceToDevice, s));
+        for (int k = levels - 2; k >= 0; --k) {
+            upsample_launch(acc, dw[k + 1], dh[k + 1], ch, dw[k], dh[k], nxt, s);
+            add_launch(nxt, lv[k], static_cast<size_t>(dw[k]) * dh[k] * ch, s);
+            std::swap(acc, nxt);
+        }
+        const size_t n0 = static_cast<size_t>(w) * h * ch;
+        LPB_CUDA(cudaMemcpyAsync(out, acc, sizeof(float) * n0,
+                                 is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+        LPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// windowed compositor buffers (shared by lp_multiband_blend and the rig)
+namespace lpb {
+
+struct ComposeBuffers {
+    int ncams = 0, levels = 0;
+    std::vector<Win> win;  // host copy
+    DBuf d_win, d_G, d_M, d_cov, d_R, d_src, d_hinv, taps;
+    std::vector<std::unique_ptr<DBuf>> bufs;
+    ComposeArgs args{};
+
+    void build(int ncams_, int levels_, int W0, int H0, const std::vector<Win>& win0, bool with_cov,
+               cudaStream_t s) {
+        ncams = ncams_;
+        levels = levels_;
+        bufs.clear();
+        win.assign(static_cast<size_t>(ncams) * levels, Win{0, 0, 0, 0});
+        args = ComposeArgs{};
+        args.ncams = ncams;
+        args.levels = levels;
+        int W = W0, H = H0;
+        for (int k = 0; k < levels; ++k) {
+            args.W[k] = W;
+            args.H[k] = H;
+            W /= 2;
+            H /= 2;
+        }
+        std::vector<float*> G(static_cast<size_t>(ncams) * levels), M(G.size());
+        std::vector<uint8_t*> cov(ncams, nullptr);
+        for (int c = 0; c < ncams; ++c) {
+            const Win w0 = win0[c];
+            for (int k = 0; k < levels; ++k) {
+                Win w;
+                w.x0 = w0.x0 >> k;
+                w.y0 = w0.y0 >> k;
+                const int x1 = std::min(args.W[k], (w0.x0 + w0.w + (1 << k) - 1) >> k);
+                const int y1 = std::min(args.H[k], (w0.y0 + w0.h + (1 << k) - 1) >> k);
+                w.w = std::max(0, x1 - w.x0);
+                w.h = std::max(0, y1 - w.y0);
+                win[c * levels + k] = w;
+                const size_t np = static_cast<size_t>(w.w) * w.h;
+                bufs.push_back(std::make_unique<DBuf>(sizeof(float) * std::max<size_t>(np, 1), s));
+                G[c * levels + k] = bufs.back()->as<float>();
+                bufs.push_back(std::make_unique<DBuf>(sizeof(float) * std::max<size_t>(np, 1), s));
+                M[c * levels + k] = bufs.back()->as<float>();
+            }
+            if (with_cov) {
+                const Win w = win[c * levels];
+                bufs.push_back(std::make_unique<DBuf>(std::max<size_t>(static_cast<size_t>(w.w) * w.h, 1), s));
+                cov[c] = bufs.back()->as<uint8_t>();
+            }
+        }
+        std::vector<float*> R(levels, nullptr);
+        for (int k = 1; k < levels; ++k) {
+            bufs.push_back(std::make_unique<DBuf>(sizeof(float) * std::max<size_t>(static_cast<size_t>(args.W[k]) * args.H[k], 1), s));
+            R[k] = bufs.back()->as<float>();
+        }
+        d_win = upload(win, s);
+        d_G = upload(G, s);
+        d_M = upload(M, s);
+        d_cov = upload(cov, s);
+        d_R = upload(R, s);
+        taps = upload(host::gaussian_kernel(1.0f), s);
+        args.win = d_win.as<Win>();
+        args.G = d_G.as<float* const>();
+        args.M = d_M.as<float* const>();
+        args.cov = d_cov.as<uint8_t* const>();
+        args.R = d_R.as<float* const>();
+        args.down_taps = taps.as<float>();
+        host_G = G;
+        host_M = M;
+    }
+    std::vector<float*> host_G, host_M;
+};
+
+static void check_levels(int w, int h, int levels) {  // gaussian_pyramid, imgops.hpp:143-150
+    if (levels < 1) throw Status(LP_TOO_MANY_LEVELS, "build_laplacian: levels must be >= 1");
+    for (int i = 1; i < levels; ++i) {
+        if (w < 2 || h < 2) throw Status(LP_TOO_MANY_LEVELS, "pyramid: image too small for requested levels");
+        w /= 2;
+        h /= 2;
+    }
+}
+
+__global__ void k_deinterleave(const float* in, int np, int ch, int c, float* out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < np) out[i] = in[static_cast<size_t>(i) * ch + c];
+}
+__global__ void k_interleave_u8(const uint8_t* in, int np, int ch, int c, uint8_t* out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < np) out[static_cast<size_t>(i) * ch + c] = in[i];
+}
+
+}  // namespace lpb
+
+extern "C" lp_status lp_multiband_blend(lp_ctx* ctx, const float* images, const float* masks, int n, int w,
+                                        int h, int ch, int levels, uint8_t* out) {
+    return guard([&] {
+        if (n < 1) throw Status(LP_MASK_MISMATCH, "multiband_blend: image/mask count mismatch");
+        check_levels(w, h, levels);
+        cudaStream_t s = ctx->stream;
+        const size_t np = static_cast<size_t>(w) * h;
+        In<float> di(images, np * ch * n, s), dm(masks, np * n, s);
+        ComposeBuffers cb;
+        std::vector<Win> full(n, Win{0, 0, w, h});
+        cb.build(n, levels, w, h, full, false, s);
+        DBuf o1(np, s);
+        Out<uint8_t> dout(out, np * ch, s);
+        cb.args.out = o1.as<uint8_t>();
+        for (int c = 0; c < n; ++c)
+            LPB_CUDA(cudaMemcpyAsync(cb.host_M[c * levels], dm.d + np * c, sizeof(float) * np, cudaMemcpyDeviceToDevice, s));
+        for (int cc = 0; cc < ch; ++cc) {
+            for (int c = 0; c < n; ++c) {
+                if (ch == 1)
+                    LPB_CUDA(cudaMemcpyAsync(cb.host_G[c * levels], di.d + np * c, sizeof(float) * np,
+                                             cudaMemcpyDeviceToDevice, s));
+                else
+                    LPB_LAUNCH(k_deinterleave, cdiv(np, 256), 256, 0, s, di.d + np * ch * c, static_cast<int>(np), ch,
+                               cc, cb.host_G[c * levels]);
+            }
+            blend_launch(cb.args, cb.win.data(), s);
+            if (ch == 1)
+                LPB_CUDA(cudaMemcpyAsync(dout.d, o1.p, np, cudaMemcpyDeviceToDevice, s));
+            else
+                LPB_LAUNCH(k_interleave_u8, cdiv(np, 256), 256, 0, s, o1.as<uint8_t>(), static_cast<int>(np), ch, cc,
+                           dout.d);
+        }
+        dout.finish(s, np * ch);
+        LPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+#include "rig.inc"

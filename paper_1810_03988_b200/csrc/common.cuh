@@ -1,0 +1,100 @@
+// common.cuh — shared device/host plumbing for the B200 stitching kernels.
+//
+// Numerics rule for the whole library: the reference is compiled for baseline
+// x86-64 (no FMA, proj/CMakeLists.txt Release flags), so every kernel is built
+// with --fmad=false and keeps the reference's operation order; float/double
+// results are then bit-identical to the CPU oracle.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "lorbpano_b200.h"
+
+namespace lpb {
+
+// Host-side error carrying an lp_status; converted at the C-ABI boundary.
+struct Status : std::runtime_error {
+    lp_status code;
+    Status(lp_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define LPB_CUDA(expr)                                                                   \
+    do {                                                                                 \
+        cudaError_t e_ = (expr);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            throw ::lpb::Status(LP_CUDA_ERROR, std::string(#expr " -> ") +               \
+                                                   cudaGetErrorString(e_));              \
+    } while (0)
+
+// every kernel launch goes through this so lp_kernel_launches() is exact
+void note_launch();
+#define LPB_LAUNCH(kernel, grid, block, smem, stream, ...)                              \
+    do {                                                                                 \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                      \
+        LPB_CUDA(cudaGetLastError());                                                    \
+        ::lpb::note_launch();                                                            \
+    } while (0)
+
+inline int cdiv(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+constexpr int kMaxLevels = 16;
+
+struct DevImage {
+    const uint8_t* p;
+    int w, h;
+};
+constexpr int kMaxCams = 64;
+
+// device-side status word: first error wins (atomicCAS from 0)
+__device__ __forceinline__ void dev_fail(int* status, int code) {
+    atomicCAS(status, 0, code);
+}
+
+// IEEE-exact helpers (explicit round-to-nearest ops, no contraction)
+__device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+// float -> orderable uint32 (total order matching float <, with -0 < +0 only
+// in bits; the reference never produces -0 responses)
+__host__ __device__ __forceinline__ uint32_t float_key(float f) {
+    uint32_t b;
+#ifdef __CUDA_ARCH__
+    b = __float_as_uint(f);
+#else
+    std::memcpy(&b, &f, 4);
+#endif
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__host__ __device__ __forceinline__ float key_float(uint32_t k) {
+    uint32_t b = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+    float f;
+#ifdef __CUDA_ARCH__
+    f = __uint_as_float(b);
+#else
+    std::memcpy(&f, &b, 4);
+#endif
+    return f;
+}
+// (response desc, y asc, x asc) as one descending 64-bit key (x, y < 65536)
+__host__ __device__ __forceinline__ uint64_t kp_key(float r, int x, int y) {
+    return (static_cast<uint64_t>(float_key(r)) << 32) |
+           static_cast<uint64_t>(0xFFFFFFFFu - ((static_cast<uint32_t>(y) << 16) | static_cast<uint32_t>(x)));
+}
+__host__ __device__ __forceinline__ void kp_unkey(uint64_t k, float* r, int* x, int* y) {
+    *r = key_float(static_cast<uint32_t>(k >> 32));
+    uint32_t yx = 0xFFFFFFFFu - static_cast<uint32_t>(k & 0xFFFFFFFFu);
+    *y = static_cast<int>(yx >> 16);
+    *x = static_cast<int>(yx & 0xFFFFu);
+}
+
+}  // namespace lpb

@@ -1,0 +1,578 @@
+// lorb.cu — L-ORB extraction kernels for sm_100a.
+//
+// Fused path (stage_detect + stage_describe, pipeline.hpp:419-469):
+//   k_detect   one CTA per 32x32 output tile of a region: the u8 tile plus a
+//              halo is staged once in shared memory;
+//              FAST-9 (lorb.hpp:141-205) runs on the tile + 1-px ring, FAST
+//              corners are compacted into a shared list, FP64 Harris
+//              (lorb.hpp:209-250) runs densely over that list from shared
+//              integer gradients, the 3x3 NMS (lorb.hpp:254-288) runs on the
+//              response map, and survivors are appended to a per-region key
+//              list with warp-aggregated atomics (ballot + popc).
+//   k_topn     one CTA per region: MSB radix select over the 64-bit key
+//              (response desc, y asc, x asc) = select_top_n's total order
+//              (lorb.hpp:291-299), then a shared-memory bitonic sort.
+//   k_describe one warp per keypoint: the 43x43 patch (BRIEF pattern half
+//              15 + blur radius 6) is blurred in shared memory with the exact
+//              separable σ=2 order of gaussian_blur (imgops.hpp:50-72), then
+//              256 ternary tests are packed into gt/lt planes with ballots
+//              (lorb.hpp:333-350). Values equal the reference's region-crop
+//              blur at every sampled point (test_lorb.cpp:301-343).
+// All FP ops are explicit round-to-nearest (no FMA), matching the reference.
+#include <cub/cub.cuh>
+
+#include "lorb.cuh"
+
+namespace lpb {
+
+// ---------------------------------------------------------------------------
+// FAST segment test on a 16-bit ring mask: a circular run of >= arc set bits
+// exists iff AND of the arc rotations is non-zero (== longest_arc >= arc).
+__device__ __forceinline__ bool has_arc(unsigned m, int arc) {
+    unsigned m32 = m | (m << 16);
+    unsigned r = m32;
+    for (int s = 1; s < arc; ++s) r &= (m32 >> s);
+    return (r & 0xFFFFu) != 0u;
+}
+
+__constant__ int c_ring_dx[16] = {0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3, -3, -3, -2, -1};
+__constant__ int c_ring_dy[16] = {-3, -3, -2, -1, 0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3};
+
+// ---------------------------------------------------------------------------
+// k_detect
+constexpr int TW = kDetTile;
+constexpr int HALO_MAX = kMaxHarrisR + 2;              // harris R + gradient 1 + NMS 1
+constexpr int IMG_MAX = TW + 2 * HALO_MAX;             // 48
+constexpr int GRAD_MAX = TW + 2 + 2 * kMaxHarrisR;     // 46
+constexpr int NMS_W = TW + 2;                          // 34
+
+__global__ void __launch_bounds__(256) k_detect(ExtractArgs a) {
+    __shared__ uint8_t s_img[IMG_MAX * IMG_MAX];
+    __shared__ short s_gx[GRAD_MAX * GRAD_MAX];
+    __shared__ short s_gy[GRAD_MAX * GRAD_MAX];
+    __shared__ float s_resp[NMS_W * NMS_W];
+    __shared__ short s_cand[NMS_W * NMS_W];
+    __shared__ double s_w[(2 * kMaxHarrisR + 1) * (2 * kMaxHarrisR + 1)];
+    __shared__ int s_ncand;
+
+    const int b = blockIdx.x;
+    int ri = 0;
+    while (ri + 1 < a.nregions && a.regions[ri + 1].tile_base <= b) ++ri;
+    const DevRegion rg = a.regions[ri];
+    const DevImage im = a.images[rg.img];
+    const int t = b - rg.tile_base;
+    const int ox = rg.x0 + (t % rg.tiles_x) * TW;
+    const int oy = rg.y0 + (t / rg.tiles_x) * TW;
+    const int R = a.harris_r;
+    const int halo = (R + 1 > 3 ? R + 1 : 3) + 1;
+    const int iw = TW + 2 * halo;
+    const int gw = TW + 2 + 2 * R;
+    const int tid = threadIdx.x;
+
+    const int K = 2 * R + 1;
+    for (int i = tid; i < K * K; i += blockDim.x) s_w[i] = a.harris_w[i];
+    if (tid == 0) s_ncand = 0;
+
+    // stage the u8 tile + halo (clamped coordinates; clamped texels are never
+    // consumed by a valid test).
+    const int gx0 = ox - halo, gy0 = oy - halo;
+    for (int i = tid; i < iw * iw; i += blockDim.x) {
+        int ly = i / iw, lx = i - ly * iw;
+        int gx = min(max(gx0 + lx, 0), im.w - 1);
+        int gy = min(max(gy0 + ly, 0), im.h - 1);
+        s_img[ly * iw + lx] = __ldg(im.p + static_cast<size_t>(gy) * im.w + gx);
+    }
+    for (int i = tid; i < NMS_W * NMS_W; i += blockDim.x) s_resp[i] = __int_as_float(0x7fc00000);
+    __syncthreads();
+
+    // integer central differences over the Harris window area
+    const int goff = halo - 1 - R;  // gradient (0,0) sits at image-local (goff, goff)
+    for (int i = tid; i < gw * gw; i += blockDim.x) {
+        int ly = i / gw, lx = i - ly * gw;
+        int ix = lx + goff, iy = ly + goff;
+        s_gx[i] = static_cast<short>(int(s_img[iy * iw + ix + 1]) - int(s_img[iy * iw + ix - 1]));
+        s_gy[i] = static_cast<short>(int(s_img[(iy + 1) * iw + ix]) - int(s_img[(iy - 1) * iw + ix]));
+    }
+
+    // FAST-9 on the tile + 1-px ring, restricted to the scan area
+    for (int i = tid; i < NMS_W * NMS_W; i += blockDim.x) {
+        int ly = i / NMS_W, lx = i - ly * NMS_W;
+        int px = ox - 1 + lx, py = oy - 1 + ly;
+        if (px < rg.x0 || px >= rg.x1 || py < rg.y0 || py >= rg.y1) continue;
+        int cx = px - gx0, cy = py - gy0;
+        int c = s_img[cy * iw + cx];
+        unsigned br = 0, dk = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            int v = s_img[(cy + c_ring_dy[k]) * iw + cx + c_ring_dx[k]];
+            br |= (v > c + a.fast_t) ? (1u << k) : 0u;
+            dk |= (v < c - a.fast_t) ? (1u << k) : 0u;
+        }
+        if (has_arc(br, a.fast_arc) || has_arc(dk, a.fast_arc)) {
+            if (px - R - 1 < 0 || px + R + 1 >= im.w || py - R - 1 < 0 || py + R + 1 >= im.h) {
+                dev_fail(a.status, LP_WINDOW_OUT_OF_BOUNDS);
+                continue;
+            }
+            int slot = atomicAdd(&s_ncand, 1);
+            s_cand[slot] = static_cast<short>(i);
+        }
+    }
+    __syncthreads();
+
+    // FP64 Harris over the compacted candidates (lorb.hpp:235-247)
+    const int nc = s_ncand;
+    const double alpha = static_cast<double>(a.alpha);
+    for (int j = tid; j < nc; j += blockDim.x) {
+        int i = s_cand[j];
+        int ly = i / NMS_W, lx = i - ly * NMS_W;
+        // gradient-local centre of this pixel
+        int gcx = lx - 1 + R + 1, gcy = ly - 1 + R + 1;
+        double sa = 0.0, sb = 0.0, sc = 0.0;
+        for (int v = -R; v <= R; ++v) {
+            const short* rx = s_gx + (gcy + v) * gw + gcx;
+            const short* ry = s_gy + (gcy + v) * gw + gcx;
+            const double* wr = s_w + (v + R) * K + R;
+            for (int u = -R; u <= R; ++u) {
+                double ix = static_cast<double>(rx[u]) / 2.0;
+                double iy = static_cast<double>(ry[u]) / 2.0;
+                double wt = wr[u];
+                sa = dadd(sa, dmul(dmul(wt, ix), ix));
+                sb = dadd(sb, dmul(dmul(wt, iy), iy));
+                sc = dadd(sc, dmul(dmul(wt, ix), iy));
+            }
+        }
+        double s = dadd(sa, sb);
+        double r = dsub(dsub(dmul(sa, sb), dmul(sc, sc)), dmul(dmul(alpha, s), s));
+        float rf = __double2float_rn(r);
+        if (rf >= a.threshold) s_resp[i] = rf;
+    }
+    __syncthreads();
+
+    // 3x3 NMS among thresholded candidates; survivors -> per-region key list
+    const int lane = tid & 31;
+    for (int base = 0; base < TW * TW; base += blockDim.x) {
+        int i = base + tid;
+        bool keep = false;
+        uint64_t key = 0;
+        if (i < TW * TW) {
+            int ly = i / TW + 1, lx = i % TW + 1;
+            float r = s_resp[ly * NMS_W + lx];
+            if (r == r) {
+                keep = true;
+#pragma unroll
+                for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        if (dx == 0 && dy == 0) continue;
+                        float o = s_resp[(ly + dy) * NMS_W + lx + dx];
+                        if (o > r || (o == r && (dy < 0 || (dy == 0 && dx < 0)))) keep = false;
+                    }
+                key = kp_key(r, ox + lx - 1, oy + ly - 1);
+            }
+        }
+        unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (m) {
+            int leader = __ffs(m) - 1;
+            unsigned pos = 0;
+            if (lane == leader) pos = atomicAdd(&a.surv_count[ri], static_cast<unsigned>(__popc(m)));
+            pos = __shfl_sync(0xffffffffu, pos, leader);
+            if (keep) {
+                unsigned slot = pos + __popc(m & ((1u << lane) - 1u));
+                if (slot < static_cast<unsigned>(a.surv_cap))
+                    a.surv[static_cast<size_t>(ri) * a.surv_cap + slot] = key;
+                else
+                    dev_fail(a.status, LP_CAPACITY_OVERFLOW);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_topn: exact per-region select_top_n via MSB radix select + bitonic sort
+__device__ void bitonic_desc(uint64_t* v, int n_pow2) {
+    for (int k = 2; k <= n_pow2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
+                int p = i ^ j;
+                if (p > i) {
+                    uint64_t x = v[i], y = v[p];
+                    bool desc = (i & k) == 0;
+                    if (desc ? (x < y) : (x > y)) {
+                        v[i] = y;
+                        v[p] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+}
+
+__global__ void __launch_bounds__(1024) k_topn(ExtractArgs a) {
+    extern __shared__ uint64_t s_keys[];  // kTopnSortCap
+    __shared__ unsigned s_hist[256];
+    __shared__ uint64_t s_prefix;
+    __shared__ int s_pbits, s_k, s_bucket, s_m;
+    const int ri = blockIdx.x;
+    const int n = min(static_cast<int>(a.surv_count[ri]), a.surv_cap);
+    const uint64_t* keys = a.surv + static_cast<size_t>(ri) * a.surv_cap;
+    const int top_n = a.top_n;
+    const int tid = threadIdx.x;
+    int m;
+    if (n <= top_n) {
+        m = n;
+        for (int i = tid; i < n; i += blockDim.x) s_keys[i] = keys[i];
+    } else {
+        if (tid == 0) {
+            s_prefix = 0;
+            s_pbits = 0;
+            s_k = top_n;
+        }
+        __syncthreads();
+        for (;;) {
+            for (int i = tid; i < 256; i += blockDim.x) s_hist[i] = 0;
+            __syncthreads();
+            const uint64_t prefix = s_prefix;
+            const int pbits = s_pbits;
+            for (int i = tid; i < n; i += blockDim.x) {
+                uint64_t k = keys[i];
+                if (pbits == 0 || (k >> (64 - pbits)) == prefix)
+                    atomicAdd(&s_hist[(k >> (56 - pbits)) & 255u], 1u);
+            }
+            __syncthreads();
+            if (tid == 0) {
+                unsigned cum = 0;
+                int sel = 0;
+                for (int d = 255; d >= 0; --d) {
+                    if (cum + s_hist[d] >= static_cast<unsigned>(s_k)) {
+                        sel = d;
+                        break;
+                    }
+                    cum += s_hist[d];
+                }
+                s_k -= static_cast<int>(cum);
+                s_bucket = static_cast<int>(s_hist[sel]);
+                s_prefix = (prefix << 8) | static_cast<uint64_t>(sel);
+                s_pbits = pbits + 8;
+            }
+            __syncthreads();
+            const int above = top_n - s_k;
+            if (above + s_bucket <= kTopnSortCap || s_pbits == 64) break;
+        }
+        if (tid == 0) s_m = 0;
+        __syncthreads();
+        const uint64_t prefix = s_prefix;
+        const int sh = 64 - s_pbits;
+        for (int i = tid; i < n; i += blockDim.x) {
+            uint64_t k = keys[i];
+            uint64_t top = sh == 64 ? 0 : (k >> sh);
+            if (top >= prefix) {
+                int slot = atomicAdd(&s_m, 1);
+                if (slot < kTopnSortCap) s_keys[slot] = k;
+            }
+        }
+        __syncthreads();
+        m = min(s_m, kTopnSortCap);
+    }
+    int p2 = 1;
+    while (p2 < m) p2 <<= 1;
+    for (int i = m + tid; i < p2; i += blockDim.x) s_keys[i] = 0;
+    __syncthreads();
+    bitonic_desc(s_keys, p2);
+    const int out_n = min(m, top_n);
+    for (int i = tid; i < out_n; i += blockDim.x) {
+        float r;
+        int x, y;
+        kp_unkey(s_keys[i], &r, &x, &y);
+        a.kp_region[static_cast<size_t>(ri) * top_n + i] = lp_keypoint{x, y, r, ri};
+    }
+    if (tid == 0) a.count_region[ri] = out_n;
+}
+
+// ---------------------------------------------------------------------------
+// k_describe: one warp per keypoint
+__global__ void __launch_bounds__(256) k_describe(ExtractArgs a, int warp_bytes) {
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    lp_pair* s_pairs = reinterpret_cast<lp_pair*>(s_dyn);
+    float* s_taps = reinterpret_cast<float*>(s_pairs + a.n_d);
+    const int warps = blockDim.x / 32;
+    unsigned char* s_warp_base = s_dyn + ((a.n_d * sizeof(lp_pair) + (2 * kMaxBlurR + 1) * 4 + 15) & ~15);
+    for (int i = threadIdx.x; i < a.n_d; i += blockDim.x) s_pairs[i] = a.pairs[i];
+    for (int i = threadIdx.x; i < 2 * a.blur_r + 1; i += blockDim.x) s_taps[i] = a.blur_taps[i];
+    if (blockIdx.x == 0 && threadIdx.x < a.nslots) {
+        int tot = 0;
+        for (int r = 0; r < a.nregions; ++r)
+            if (a.regions[r].out_slot == static_cast<int>(threadIdx.x)) tot += a.count_region[r];
+        a.slot_count[threadIdx.x] = tot;
+    }
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gslot = blockIdx.x * warps + warp;
+    const int ri = gslot / a.top_n, i = gslot - ri * a.top_n;
+    if (ri >= a.nregions || i >= a.count_region[ri]) return;
+    const DevRegion rg = a.regions[ri];
+    const DevImage im = a.images[rg.img];
+    const lp_keypoint kp = a.kp_region[static_cast<size_t>(ri) * a.top_n + i];
+    int off = 0;
+    for (int r = 0; r < ri; ++r)
+        if (a.regions[r].out_slot == rg.out_slot) off += a.count_region[r];
+    const int idx = off + i;
+    const int P = a.patch_half, RB = a.blur_r;
+    const int pw = 2 * P + 1, iw = pw + 2 * RB;
+
+    // smoothed_crop bounds (lorb.hpp:371-375) for the PatchOutOfBounds test (336-338)
+    const int margin = P + RB;
+    const int cx0 = max(0, rg.rx0 - margin), cy0 = max(0, rg.ry0 - margin);
+    const int cx1 = min(im.w, rg.rx1 + margin), cy1 = min(im.h, rg.ry1 + margin);
+    if (kp.x - P < cx0 || kp.x + P >= cx1 || kp.y - P < cy0 || kp.y + P >= cy1) {
+        if (lane == 0) dev_fail(a.status, LP_PATCH_OUT_OF_BOUNDS);
+        return;
+    }
+
+    unsigned char* sw = s_warp_base + static_cast<size_t>(warp) * warp_bytes;
+    uint8_t* s_in = sw;                                                   // iw x iw
+    float* s_tmp = reinterpret_cast<float*>(sw + ((iw * iw + 15) & ~15));  // iw rows x pw cols
+    float* s_S = s_tmp + iw * pw;                                         // pw x pw
+    const int bx = kp.x - P - RB, by = kp.y - P - RB;
+    for (int j = lane; j < iw * iw; j += 32) {
+        int ly = j / iw, lx = j - ly * iw;
+        int gx = min(max(bx + lx, 0), im.w - 1), gy = min(max(by + ly, 0), im.h - 1);
+        s_in[j] = __ldg(im.p + static_cast<size_t>(gy) * im.w + gx);
+    }
+    __syncwarp();
+    // horizontal pass: every staged row, the pw patch columns
+    for (int j = lane; j < iw * pw; j += 32) {
+        int ly = j / pw, lx = j - ly * pw;
+        const uint8_t* row = s_in + ly * iw + lx;
+        float acc = 0.0f;
+        for (int q = 0; q <= 2 * RB; ++q) acc = fadd(acc, fmul(s_taps[q], static_cast<float>(row[q])));
+        s_tmp[j] = acc;
+    }
+    __syncwarp();
+    // vertical pass
+    for (int j = lane; j < pw * pw; j += 32) {
+        int ly = j / pw, lx = j - ly * pw;
+        float acc = 0.0f;
+        for (int q = 0; q <= 2 * RB; ++q) acc = fadd(acc, fmul(s_taps[q], s_tmp[(ly + q) * pw + lx]));
+        s_S[j] = acc;
+    }
+    __syncwarp();
+    // ternary tests -> gt / lt bitplanes
+    const int W = (a.n_d + 63) / 64;
+    uint64_t* d = a.desc_out + (static_cast<size_t>(rg.out_slot) * a.cap_slot + idx) * 2 * W;
+    for (int w = 0; w < W; ++w) {
+        unsigned g[2], l[2];
+        for (int h = 0; h < 2; ++h) {
+            int pi = w * 64 + h * 32 + lane;
+            bool gt = false, lt = false;
+            if (pi < a.n_d) {
+                lp_pair pr = s_pairs[pi];
+                float ip = s_S[(P + pr.py) * pw + P + pr.px];
+                float iq = s_S[(P + pr.qy) * pw + P + pr.qx];
+                gt = ip > iq;
+                lt = ip < iq;
+            }
+            g[h] = __ballot_sync(0xffffffffu, gt);
+            l[h] = __ballot_sync(0xffffffffu, lt);
+        }
+        if (lane == 0) {
+            d[w] = static_cast<uint64_t>(g[0]) | (static_cast<uint64_t>(g[1]) << 32);
+            d[W + w] = static_cast<uint64_t>(l[0]) | (static_cast<uint64_t>(l[1]) << 32);
+        }
+    }
+    if (lane == 0) a.kp_out[static_cast<size_t>(rg.out_slot) * a.cap_slot + idx] = kp;
+}
+
+void extract_launch(const ExtractArgs& a, cudaStream_t s) {
+    if (a.nregions == 0) return;
+    LPB_CUDA(cudaMemsetAsync(a.surv_count, 0, sizeof(unsigned) * a.nregions, s));
+    if (a.total_tiles > 0) LPB_LAUNCH(k_detect, a.total_tiles, 256, 0, s, a);
+    const int topn_smem = kTopnSortCap * sizeof(uint64_t);
+    LPB_CUDA(cudaFuncSetAttribute(k_topn, cudaFuncAttributeMaxDynamicSharedMemorySize, topn_smem));
+    LPB_LAUNCH(k_topn, a.nregions, 1024, topn_smem, s, a);
+    const int P = a.patch_half, RB = a.blur_r;
+    const int pw = 2 * P + 1, iw = pw + 2 * RB;
+    const int warp_bytes = (((iw * iw + 15) & ~15) + (iw * pw + pw * pw) * 4 + 15) & ~15;
+    const int head = (a.n_d * static_cast<int>(sizeof(lp_pair)) + (2 * kMaxBlurR + 1) * 4 + 15) & ~15;
+    int warps = 8;
+    while (warps > 1 && head + warps * warp_bytes > 200 * 1024) warps >>= 1;
+    const int smem = head + warps * warp_bytes;
+    if (smem > 227 * 1024) throw Status(LP_BAD_PARAMS, "describe: patch too large for shared memory");
+    LPB_CUDA(cudaFuncSetAttribute(k_describe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int total = a.nregions * a.top_n;
+    LPB_LAUNCH(k_describe, cdiv(total, warps), warps * 32, smem, s, a, warp_bytes);
+}
+
+// ---------------------------------------------------------------------------
+// Stage-isolated primitives
+__global__ void k_fast_flags(const uint8_t* img, int w, int h, int x0, int y0, int x1, int y1,
+                             int t, int arc, uint8_t* flags) {
+    const int sw = x1 - x0;
+    const long long n = static_cast<long long>(sw) * (y1 - y0);
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        int x = x0 + static_cast<int>(i % sw), y = y0 + static_cast<int>(i / sw);
+        int c = img[static_cast<size_t>(y) * w + x];
+        unsigned br = 0, dk = 0;
+        for (int k = 0; k < 16; ++k) {
+            int v = img[static_cast<size_t>(y + c_ring_dy[k]) * w + x + c_ring_dx[k]];
+            br |= (v > c + t) ? (1u << k) : 0u;
+            dk |= (v < c - t) ? (1u << k) : 0u;
+        }
+        flags[i] = (has_arc(br, arc) || has_arc(dk, arc)) ? 1 : 0;
+    }
+}
+void fast_flags_launch(const uint8_t* img, int w, int h, int x0, int y0, int x1, int y1, int t,
+                       int arc, uint8_t* flags, cudaStream_t s) {
+    long long n = static_cast<long long>(x1 - x0) * (y1 - y0);
+    LPB_LAUNCH(k_fast_flags, std::min<long long>(cdiv(n, 256), 148 * 16), 256, 0, s, img, w, h,
+               x0, y0, x1, y1, t, arc, flags);
+}
+
+__global__ void k_harris_points(const uint8_t* img, int w, int h, const int* xy, int n,
+                                const double* wts, int R, float alpha, float* out, int* status) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int px = xy[2 * p], py = xy[2 * p + 1];
+    if (px - R - 1 < 0 || px + R + 1 >= w || py - R - 1 < 0 || py + R + 1 >= h) {
+        dev_fail(status, LP_WINDOW_OUT_OF_BOUNDS);
+        return;
+    }
+    const int K = 2 * R + 1;
+    double sa = 0.0, sb = 0.0, sc = 0.0;
+    for (int v = -R; v <= R; ++v)
+        for (int u = -R; u <= R; ++u) {
+            const int x = px + u, y = py + v;
+            const size_t o = static_cast<size_t>(y) * w + x;
+            double ix = (static_cast<double>(img[o + 1]) - img[o - 1]) / 2.0;
+            double iy = (static_cast<double>(img[o + w]) - img[o - w]) / 2.0;
+            double wt = wts[(v + R) * K + (u + R)];
+            sa = dadd(sa, dmul(dmul(wt, ix), ix));
+            sb = dadd(sb, dmul(dmul(wt, iy), iy));
+            sc = dadd(sc, dmul(dmul(wt, ix), iy));
+        }
+    double s = dadd(sa, sb);
+    out[p] = __double2float_rn(dsub(dsub(dmul(sa, sb), dmul(sc, sc)),
+                                    dmul(dmul(static_cast<double>(alpha), s), s)));
+}
+void harris_points_launch(const uint8_t* img, int w, int h, const int* xy, int n,
+                          const double* wts, int r, float alpha, float* out, int* status,
+                          cudaStream_t s) {
+    if (n == 0) return;
+    LPB_LAUNCH(k_harris_points, cdiv(n, 128), 128, 0, s, img, w, h, xy, n, wts, r, alpha, out,
+               status);
+}
+
+// generic nms (lorb.hpp:254-288): dense grid over the bbox, last index wins
+__global__ void k_nms_scatter(const lp_keypoint* in, int n, int minx, int miny, int gw, int* grid) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    atomicMax(&grid[static_cast<size_t>(in[i].y - miny) * gw + (in[i].x - minx)], i);
+}
+__global__ void k_nms_check(const lp_keypoint* in, int n, int radius, int minx, int miny, int gw,
+                            int gh, const int* grid, uint8_t* keep) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const lp_keypoint k = in[i];
+    bool wins = true;
+    for (int dy = -radius; dy <= radius && wins; ++dy)
+        for (int dx = -radius; dx <= radius && wins; ++dx) {
+            if (dx == 0 && dy == 0) continue;
+            int gx = k.x - minx + dx, gy = k.y - miny + dy;
+            if (gx < 0 || gx >= gw || gy < 0 || gy >= gh) continue;
+            int j = grid[static_cast<size_t>(gy) * gw + gx];
+            if (j < 0) continue;
+            const lp_keypoint o = in[j];
+            if (o.response > k.response ||
+                (o.response == k.response && (o.y < k.y || (o.y == k.y && o.x < k.x))))
+                wins = false;
+        }
+    keep[i] = wins ? 1 : 0;
+}
+void nms_generic_launch(const lp_keypoint* in, int n, int radius, int minx, int miny, int gw,
+                        int gh, int* grid, uint8_t* keep, cudaStream_t s) {
+    LPB_CUDA(cudaMemsetAsync(grid, 0xff, sizeof(int) * static_cast<size_t>(gw) * gh, s));
+    LPB_LAUNCH(k_nms_scatter, cdiv(n, 256), 256, 0, s, in, n, minx, miny, gw, grid);
+    LPB_LAUNCH(k_nms_check, cdiv(n, 256), 256, 0, s, in, n, radius, minx, miny, gw, gh, grid, keep);
+}
+
+// generic separable blur (imgops.hpp:50-72), global-memory form
+__global__ void k_blur_h(const float* in, float* out, int w, int h, int ch, const float* taps, int r) {
+    long long n = static_cast<long long>(w) * h * ch;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        int c = static_cast<int>(i % ch);
+        long long p = i / ch;
+        int x = static_cast<int>(p % w), y = static_cast<int>(p / w);
+        float acc = 0.0f;
+        for (int q = -r; q <= r; ++q) {
+            int xx = min(max(x + q, 0), w - 1);
+            acc = fadd(acc, fmul(taps[q + r], in[(static_cast<size_t>(y) * w + xx) * ch + c]));
+        }
+        out[i] = acc;
+    }
+}
+__global__ void k_blur_v(const float* in, float* out, int w, int h, int ch, const float* taps, int r) {
+    long long n = static_cast<long long>(w) * h * ch;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        int c = static_cast<int>(i % ch);
+        long long p = i / ch;
+        int x = static_cast<int>(p % w), y = static_cast<int>(p / w);
+        float acc = 0.0f;
+        for (int q = -r; q <= r; ++q) {
+            int yy = min(max(y + q, 0), h - 1);
+            acc = fadd(acc, fmul(taps[q + r], in[(static_cast<size_t>(yy) * w + x) * ch + c]));
+        }
+        out[i] = acc;
+    }
+}
+void blur_launch(const float* in, float* tmp, float* out, int w, int h, int ch, const float* taps,
+                 int r, cudaStream_t s) {
+    long long n = static_cast<long long>(w) * h * ch;
+    int g = static_cast<int>(std::min<long long>(cdiv(n, 256), 148 * 32));
+    LPB_LAUNCH(k_blur_h, g, 256, 0, s, in, tmp, w, h, ch, taps, r);
+    LPB_LAUNCH(k_blur_v, g, 256, 0, s, tmp, out, w, h, ch, taps, r);
+}
+
+// brief_descriptor on a pre-smoothed image (lorb.hpp:333-350): warp per keypoint
+__global__ void k_brief_generic(const float* sm, int w, int h, const lp_keypoint* kps, int n,
+                                const lp_pair* pairs, int n_d, int ph, uint64_t* out, int* status) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= n) return;
+    const lp_keypoint kp = kps[warp];
+    if (kp.x - ph < 0 || kp.x + ph >= w || kp.y - ph < 0 || kp.y + ph >= h) {
+        if (lane == 0) dev_fail(status, LP_PATCH_OUT_OF_BOUNDS);
+        return;
+    }
+    const int W = (n_d + 63) / 64;
+    uint64_t* d = out + static_cast<size_t>(warp) * 2 * W;
+    for (int wd = 0; wd < W; ++wd) {
+        unsigned g[2], l[2];
+        for (int hh = 0; hh < 2; ++hh) {
+            int pi = wd * 64 + hh * 32 + lane;
+            bool gt = false, lt = false;
+            if (pi < n_d) {
+                lp_pair p = pairs[pi];
+                float ip = sm[static_cast<size_t>(kp.y + p.py) * w + kp.x + p.px];
+                float iq = sm[static_cast<size_t>(kp.y + p.qy) * w + kp.x + p.qx];
+                gt = ip > iq;
+                lt = ip < iq;
+            }
+            g[hh] = __ballot_sync(0xffffffffu, gt);
+            l[hh] = __ballot_sync(0xffffffffu, lt);
+        }
+        if (lane == 0) {
+            d[wd] = static_cast<uint64_t>(g[0]) | (static_cast<uint64_t>(g[1]) << 32);
+            d[W + wd] = static_cast<uint64_t>(l[0]) | (static_cast<uint64_t>(l[1]) << 32);
+        }
+    }
+}
+void brief_generic_launch(const float* sm, int w, int h, const lp_keypoint* kps, int n,
+                          const lp_pair* pairs, int n_d, int ph, uint64_t* out, int* status,
+                          cudaStream_t s) {
+    if (n == 0) return;
+    LPB_LAUNCH(k_brief_generic, cdiv(n, 4), 128, 0, s, sm, w, h, kps, n, pairs, n_d, ph, out, status);
+}
+
+}  // namespace lpb

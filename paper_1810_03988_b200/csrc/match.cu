@@ -1,0 +1,198 @@
+// match.cu — multi-probe LSH matching with Hamming ratio test (matchlsh.hpp).
+//
+// The reference builds L bucket tables over the train set and, per query,
+// probes T buckets per table (matchlsh.hpp:132-159). On the device the same
+// candidate set is produced by the equivalent pairwise predicate (SURVEY §8(a)
+// H16, verified): train j is a candidate of query q iff for some table t,
+// key_t(q) XOR key_t(j) is one of the probe masks. Candidates are deduplicated
+// by construction, distances are __popc over the gt/lt planes
+// (matchlsh.hpp:25-33), and each warp keeps the lexicographic top-2
+// (distance, train_id) of one query, which is all the ratio test
+// (matchlsh.hpp:183-186) needs. A per-pair CTA then orders accepted matches by
+// (quality desc, query_id asc) = (distance asc, query_id asc) with a bitonic
+// sort and emits the Correspondence list for PROSAC (pipeline.hpp:480-488).
+#include "match.cuh"
+
+namespace lpb {
+
+__global__ void k_lsh_keys(MatchArgs a) {
+    const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+    const int slot = gi / a.cap, i = gi - slot * a.cap;
+    if (slot >= a.nslots || i >= a.counts[slot]) return;
+    const int W = (a.n_d + 63) / 64;
+    const uint64_t* d = a.desc + (static_cast<size_t>(slot) * a.cap + i) * 2 * W;
+    for (int t = 0; t < a.tables; ++t) {
+        uint64_t key = 0;
+        for (int b = 0; b < a.bits; ++b) {
+            const int p = a.bitpos[t * a.bits + b];
+            const uint64_t* plane = p < a.n_d ? d : d + W;
+            const int bit = p < a.n_d ? p : p - a.n_d;
+            key |= ((plane[bit >> 6] >> (bit & 63)) & 1ull) << b;
+        }
+        a.keys[(static_cast<size_t>(slot) * a.cap + i) * a.tables + t] = key;
+    }
+}
+
+__device__ __forceinline__ bool in_probe_set(uint64_t x, const MatchArgs& a) {
+    const int p = __popcll(x);
+    if (p <= a.full_card) return true;
+    if (p != a.full_card + 1) return false;
+    for (int i = 0; i < a.npartial; ++i)
+        if (a.partial[i] == x) return true;
+    return false;
+}
+
+// lexicographic (distance, id) insert into a top-2
+__device__ __forceinline__ void top2_insert(int d, int j, int& d0, int& j0, int& d1, int& j1) {
+    if (d < d0 || (d == d0 && j < j0)) {
+        d1 = d0;
+        j1 = j0;
+        d0 = d;
+        j0 = j;
+    } else if (d < d1 || (d == d1 && j < j1)) {
+        d1 = d;
+        j1 = j;
+    }
+}
+
+constexpr int kQueriesPerWarp = 4;
+constexpr int kMaxW = 8;  // n_d <= 512
+
+__global__ void __launch_bounds__(256) k_match_query(MatchArgs a) {
+    const int pair = blockIdx.y;
+    const int qs = a.qslot0 + pair, ts = a.tslot0 + pair;
+    const int nq = a.counts[qs], nt = a.counts[ts];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int W = (a.n_d + 63) / 64;
+    const uint64_t* tkeys = a.keys + static_cast<size_t>(ts) * a.cap * a.tables;
+    const uint64_t* tdesc = a.desc + static_cast<size_t>(ts) * a.cap * 2 * W;
+    const int q_base = (blockIdx.x * (blockDim.x >> 5) + warp) * kQueriesPerWarp;
+    for (int qq = 0; qq < kQueriesPerWarp; ++qq) {
+        const int q = q_base + qq;
+        if (q >= nq) return;
+        uint64_t qk[8];
+        for (int t = 0; t < a.tables && t < 8; ++t)
+            qk[t] = a.keys[(static_cast<size_t>(qs) * a.cap + q) * a.tables + t];
+        uint64_t qd[2 * kMaxW];
+        const uint64_t* qdp = a.desc + (static_cast<size_t>(qs) * a.cap + q) * 2 * W;
+        for (int w = 0; w < 2 * W; ++w) qd[w] = qdp[w];
+        const int BIG = 0x7fffffff;
+        int d0 = BIG, j0 = BIG, d1 = BIG, j1 = BIG;
+        for (int j = lane; j < nt; j += 32) {
+            bool cand = false;
+            for (int t = 0; t < a.tables; ++t) {
+                const uint64_t tk = tkeys[static_cast<size_t>(j) * a.tables + t];
+                const uint64_t qkt = t < 8 ? qk[t] : a.keys[(static_cast<size_t>(qs) * a.cap + q) * a.tables + t];
+                if (in_probe_set(qkt ^ tk, a)) {
+                    cand = true;
+                    break;
+                }
+            }
+            if (!cand) continue;
+            const uint64_t* td = tdesc + static_cast<size_t>(j) * 2 * W;
+            int d = 0;
+            for (int w = 0; w < 2 * W; ++w) d += __popcll(qd[w] ^ td[w]);
+            if (d <= a.max_distance) top2_insert(d, j, d0, j0, d1, j1);
+        }
+        // warp merge of the per-lane top-2 lists
+        for (int off = 16; off > 0; off >>= 1) {
+            int od0 = __shfl_xor_sync(0xffffffffu, d0, off), oj0 = __shfl_xor_sync(0xffffffffu, j0, off);
+            int od1 = __shfl_xor_sync(0xffffffffu, d1, off), oj1 = __shfl_xor_sync(0xffffffffu, j1, off);
+            top2_insert(od0, oj0, d0, j0, d1, j1);
+            top2_insert(od1, oj1, d0, j0, d1, j1);
+        }
+        if (lane == 0) {
+            int4 r;
+            r.x = j0 == BIG ? -1 : j0;
+            r.y = d0;
+            r.z = j1 == BIG ? -1 : d1;  // second-best distance, or -1 when < 2 hits
+            r.w = 0;
+            a.qres[static_cast<size_t>(pair) * a.cap + q] = r;
+        }
+    }
+}
+
+// per pair: ratio test, (distance, query) order, matches + correspondences
+__global__ void __launch_bounds__(1024) k_match_finalize(MatchArgs a) {
+    extern __shared__ uint32_t s_k[];
+    __shared__ int s_n;
+    const int pair = blockIdx.x;
+    const int qs = a.qslot0 + pair, ts = a.tslot0 + pair;
+    const int nq = a.counts[qs], nt = a.counts[ts];
+    if (threadIdx.x == 0) {
+        s_n = 0;
+        if (nq == 0 || nt == 0) dev_fail(a.pair_status + pair, LP_EMPTY_INPUT);
+    }
+    __syncthreads();
+    if (nq == 0 || nt == 0) {
+        if (threadIdx.x == 0) a.match_counts[pair] = 0;
+        return;
+    }
+    for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+        const int4 r = a.qres[static_cast<size_t>(pair) * a.cap + q];
+        if (r.x < 0) continue;
+        if (r.z >= 0 && !(static_cast<float>(r.y) < fmul(a.ratio, static_cast<float>(r.z)))) continue;
+        const int slot = atomicAdd(&s_n, 1);
+        s_k[slot] = (static_cast<uint32_t>(r.y) << 21) | static_cast<uint32_t>(q);
+    }
+    __syncthreads();
+    const int n = s_n;
+    int p2 = 1;
+    while (p2 < n) p2 <<= 1;
+    for (int i = n + threadIdx.x; i < p2; i += blockDim.x) s_k[i] = 0xffffffffu;
+    __syncthreads();
+    for (int k = 2; k <= p2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+                int p = i ^ j;
+                if (p > i) {
+                    uint32_t x = s_k[i], y = s_k[p];
+                    bool asc = (i & k) == 0;
+                    if (asc ? (x > y) : (x < y)) {
+                        s_k[i] = y;
+                        s_k[p] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    const float denom = fmul(2.0f, static_cast<float>(a.n_d));
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int q = static_cast<int>(s_k[i] & 0x1FFFFFu);
+        const int d = static_cast<int>(s_k[i] >> 21);
+        const int4 r = a.qres[static_cast<size_t>(pair) * a.cap + q];
+        lp_match m;
+        m.query_id = q;
+        m.train_id = r.x;
+        m.distance = d;
+        m.quality = fsub(1.0f, __fdiv_rn(static_cast<float>(d), denom));
+        a.matches[static_cast<size_t>(pair) * a.cap + i] = m;
+        const lp_keypoint s = a.kps[static_cast<size_t>(qs) * a.cap + q];
+        const lp_keypoint t = a.kps[static_cast<size_t>(ts) * a.cap + r.x];
+        lp_corr c;
+        c.sx = static_cast<double>(s.x);
+        c.sy = static_cast<double>(s.y);
+        c.dx = static_cast<double>(t.x);
+        c.dy = static_cast<double>(t.y);
+        c.quality = m.quality;
+        c.pad_ = 0;
+        a.corr[static_cast<size_t>(pair) * a.cap + i] = c;
+    }
+    if (threadIdx.x == 0) a.match_counts[pair] = n;
+}
+
+void match_launch(const MatchArgs& a, cudaStream_t s) {
+    if (a.npairs <= 0) return;
+    if (a.n_d > 64 * kMaxW) throw Status(LP_BAD_PARAMS, "match: n_d too large");
+    if (a.cap >= (1 << 21)) throw Status(LP_BAD_PARAMS, "match: too many descriptors");
+    LPB_LAUNCH(k_lsh_keys, cdiv(static_cast<long long>(a.nslots) * a.cap, 256), 256, 0, s, a);
+    dim3 grid(cdiv(a.cap, 8 * kQueriesPerWarp), a.npairs);
+    LPB_LAUNCH(k_match_query, grid, 256, 0, s, a);
+    int p2 = 1;
+    while (p2 < a.cap) p2 <<= 1;
+    const int smem = p2 * 4;
+    LPB_CUDA(cudaFuncSetAttribute(k_match_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    LPB_LAUNCH(k_match_finalize, a.npairs, 1024, smem, s, a);
+}
+
+}  // namespace lpb

@@ -1,0 +1,32 @@
+// match.cuh — device LSH matcher (matchlsh.hpp:173-193), batched over camera pairs.
+#pragma once
+#include "common.cuh"
+
+namespace lpb {
+
+struct MatchArgs {
+    int npairs;
+    int qslot0, tslot0;         // pair p queries slot qslot0+p against train slot tslot0+p
+    int nslots;                 // descriptor slots that need LSH keys
+    const uint64_t* desc;       // nslots * cap * 2W
+    const lp_keypoint* kps;     // nslots * cap
+    const int* counts;          // nslots
+    int cap, n_d;
+    const int* bitpos;          // tables * bits
+    int tables, bits;
+    int full_card;              // probe set: all masks with popcount <= full_card ...
+    const uint64_t* partial;    // ... plus these
+    int npartial;
+    int max_distance;
+    float ratio;
+    uint64_t* keys;             // nslots * cap * tables (scratch)
+    int4* qres;                 // npairs * cap (scratch)
+    lp_match* matches;          // npairs * cap
+    lp_corr* corr;              // npairs * cap
+    int* match_counts;          // npairs
+    int* pair_status;           // npairs
+};
+
+void match_launch(const MatchArgs& a, cudaStream_t s);
+
+}  // namespace lpb

@@ -1,0 +1,198 @@
+"""Python host side of the B200 stitching path: loads the in-tree CUDA library
+(_lib/liblorbpano_b200.so) and exposes the reference's function names through
+the C-ABI. There is no CPU fallback: if the library or a GPU is missing, the
+calls fail loudly (LorbError NoDevice / ImportError)."""
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+from . import abi
+from .api import AbiWrapper, _ptr
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "liblorbpano_b200.so")
+CSRC = os.path.join(HERE, "csrc")
+
+_lock = threading.Lock()
+_lib = None
+
+
+def build(jobs=8):
+    """Compile csrc/*.cu for sm_100a into _lib/liblorbpano_b200.so (make, in-tree)."""
+    r = subprocess.run(["make", "-s", f"-j{jobs}", "-f", os.path.join(CSRC, "Makefile")],
+                       cwd=CSRC, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("CUDA build failed:\n" + r.stdout[-4000:] + r.stderr[-4000:])
+    return LIB_PATH
+
+
+def load():
+    """The product library (built in-tree if absent). Raises if it cannot be had."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            build()
+        lib = C.CDLL(LIB_PATH)
+        abi.bind(lib, "lp_", with_ctx=True)
+        P = C.c_void_p
+        lib.lp_ctx_create.argtypes = [C.c_int, C.POINTER(P)]
+        lib.lp_ctx_create.restype = C.c_int
+        lib.lp_ctx_destroy.argtypes = [P]
+        lib.lp_ctx_destroy.restype = None
+        lib.lp_ctx_set_stream.argtypes = [P, P]
+        lib.lp_ctx_set_stream.restype = C.c_int
+        lib.lp_kernel_launches.argtypes = []
+        lib.lp_kernel_launches.restype = C.c_uint64
+        lib.lp_params_default.argtypes = [C.POINTER(abi.Params)]
+        lib.lp_params_default.restype = None
+        lib.lp_rig_create.argtypes = [P, C.c_int, C.c_int, C.c_int, C.POINTER(abi.Params), C.POINTER(P)]
+        lib.lp_rig_create.restype = C.c_int
+        lib.lp_rig_destroy.argtypes = [P]
+        lib.lp_rig_destroy.restype = None
+        lib.lp_rig_stitch.argtypes = [P, P, C.c_uint64, C.POINTER(abi.FrameOut)]
+        lib.lp_rig_stitch.restype = C.c_int
+        lib.lp_rig_panorama_capacity.argtypes = [P]
+        lib.lp_rig_panorama_capacity.restype = C.c_size_t
+        lib.lp_rig_stream.argtypes = [P]
+        lib.lp_rig_stream.restype = P
+        _lib = lib
+        return lib
+
+
+def kernel_launches():
+    return int(load().lp_kernel_launches())
+
+
+def _check(lib, st):
+    if st != 0:
+        raise abi.LorbError(st, lib.lp_last_error().decode())
+
+
+class Lorb(AbiWrapper):
+    """The reference's L1 API (lorb/matchlsh/homography/compose/imgops) on the GPU."""
+
+    def __init__(self, device=0):
+        self.lib = load()
+        self.prefix = "lp_"
+        ctx = C.c_void_p()
+        _check(self.lib, self.lib.lp_ctx_create(device, C.byref(ctx)))
+        self.ctx = ctx
+        self.ctx_args = (ctx,)
+
+    def close(self):
+        if self.ctx:
+            self.lib.lp_ctx_destroy(self.ctx)
+            self.ctx = None
+            self.ctx_args = ()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def default_params(self):
+        p = abi.Params()
+        self.lib.lp_params_default(C.byref(p))
+        return p
+
+    def stitch_frame(self, images, params, frame_index=0, pano_cap=None):
+        """One frame through a fresh engine (the oracles' stitch_frame)."""
+        h, w = images[0].shape[:2]
+        rig = Rig(self, len(images), w, h, params)
+        try:
+            return rig.stitch(images, frame_index, pano_cap=pano_cap, details=True)
+        finally:
+            rig.close()
+
+
+class Rig:
+    """StitchEngine for a chain of identical cameras (pipeline.hpp:341-721) on one GPU."""
+
+    def __init__(self, lorb, ncams, w, h, params):
+        self.lorb = lorb
+        self.lib = lorb.lib
+        self.ncams, self.w, self.h = ncams, w, h
+        self.params = params
+        r = C.c_void_p()
+        _check(self.lib, self.lib.lp_rig_create(lorb.ctx, ncams, w, h, C.byref(params), C.byref(r)))
+        self.rig = r
+
+    def close(self):
+        if self.rig:
+            self.lib.lp_rig_destroy(self.rig)
+            self.rig = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self):
+        return self.lib.lp_rig_stream(self.rig)
+
+    def panorama_capacity(self):
+        return int(self.lib.lp_rig_panorama_capacity(self.rig))
+
+    def stitch_raw(self, image_ptrs, frame_index, fo):
+        """Zero-copy call: image_ptrs = list of addresses (host or device), fo a FrameOut."""
+        arr = (C.c_void_p * self.ncams)(*image_ptrs)
+        _check(self.lib, self.lib.lp_rig_stitch(self.rig, arr, frame_index, C.byref(fo)))
+
+    def stitch(self, images, frame_index=0, pano_cap=None, details=False):
+        ptrs = []
+        keep = []
+        for im in images:
+            if hasattr(im, "data_ptr"):
+                ptrs.append(im.data_ptr())
+            else:
+                a = np.ascontiguousarray(im, np.uint8)
+                keep.append(a)
+                ptrs.append(a.ctypes.data)
+        p = self.params
+        ncams = self.ncams
+        pano_cap = pano_cap or self.panorama_capacity()
+        pano = np.zeros(pano_cap, np.uint8)
+        homs = (abi.Homography * ncams)()
+        fo = abi.FrameOut()
+        fo.panorama = pano.ctypes.data_as(abi.c_u8p)
+        fo.pano_cap = pano_cap
+        fo.homographies = homs
+        if details:
+            cap_kp = 2 * p.extraction.top_n
+            W = (p.extraction.n_d + 63) // 64
+            kpc = np.zeros(ncams, np.int32)
+            kps = np.zeros((ncams, cap_kp, 4), np.int32)
+            desc = np.zeros((ncams, cap_kp, 2 * W), np.uint64)
+            mc = np.zeros(max(ncams - 1, 1), np.int32)
+            mt = np.zeros((max(ncams - 1, 1), cap_kp, 4), np.int32)
+            fo.kp_counts = kpc.ctypes.data_as(abi.c_intp)
+            fo.keypoints = kps.ctypes.data_as(C.POINTER(abi.Keypoint))
+            fo.descriptors = desc.ctypes.data_as(abi.c_u64p)
+            fo.cap_kp = cap_kp
+            fo.match_counts = mc.ctypes.data_as(abi.c_intp)
+            fo.matches = mt.ctypes.data_as(C.POINTER(abi.Match))
+            fo.cap_matches = cap_kp
+        self.stitch_raw(ptrs, frame_index, fo)
+        cv = fo.canvas
+        out = dict(
+            canvas=(cv.width, cv.height, cv.origin_x, cv.origin_y),
+            panorama=pano[:cv.width * cv.height].reshape(cv.height, cv.width).copy(),
+            homographies=np.array([homs[i].h[:] for i in range(ncams)]).reshape(ncams, 3, 3),
+            estimated=bool(fo.estimated),
+            stage_ms=list(fo.stage_ms),
+        )
+        if details:
+            out.update(
+                keypoints=[kps[c, :kpc[c]].copy() for c in range(ncams)],
+                descriptors=[desc[c, :kpc[c]].copy() for c in range(ncams)],
+                matches=[mt[q, :mc[q]].copy() for q in range(ncams - 1)],
+            )
+        return out

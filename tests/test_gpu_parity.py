@@ -1,0 +1,345 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the C restatement
+oracle on identical seeded inputs. Integer/byte/index outputs and the FP32
+rasters must be bit-identical; homographies are compared bit-exact too (the
+device DLT replays the oracle's canonical SVD) with the reference's own
+tolerance (frobenius_rel < 1e-4, test_homography.cpp:12-19) as the floor."""
+import numpy as np
+import pytest
+
+from tests.conftest import chain_cameras, rand_image
+from tests.golden.make_golden import prosac_data
+
+pytestmark = pytest.mark.gpu
+
+
+def frob_rel(a, b):
+    a = np.asarray(a, float) / a[2, 2]
+    b = np.asarray(b, float) / b[2, 2]
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+# ---------------------------------------------------------------- L-ORB
+@pytest.mark.parametrize("seed", range(5))
+@pytest.mark.parametrize("arc", [9, 12, 16])
+def test_fast_corners(lp, orc, seed, arc):
+    img = rand_image(97, 83, seed)
+    for region, t in (((0, 0, 97, 83, 0), 20), ((10, 7, 60, 70, 1), 5 + seed)):
+        a = lp.fast_corners(img, region, t, arc)
+        b = orc.fast_corners(img, region, t, arc)
+        assert np.array_equal(a, b)
+
+
+def test_fast_corners_texture_and_cap(lp, orc):
+    tex = orc.texture(400, 300, 3)
+    a = lp.fast_corners(tex, (15, 15, 385, 285, 0))
+    b = orc.fast_corners(tex, (15, 15, 385, 285, 0))
+    assert len(a) > 1000 and np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("sigma", [1.0, 0.7, 1.6])
+def test_harris(lp, orc, sigma):
+    img = orc.texture(120, 90, 9)
+    r = int(np.ceil(3 * sigma)) + 1
+    ys, xs = np.mgrid[r:90 - r:3, r:120 - r:2]
+    xy = np.stack([xs.ravel(), ys.ravel()], 1).astype(np.int32)
+    a = lp.harris_response(img, xy, 0.04, sigma)
+    b = orc.harris_response(img, xy, 0.04, sigma)
+    assert a.tobytes() == b.tobytes()
+
+
+def test_nms_topn(lp, orc):
+    img = orc.texture(200, 150, 4)
+    xy = orc.fast_corners(img, (10, 10, 190, 140, 0))
+    resp = orc.harris_response(img, xy)
+    kp = np.zeros((len(xy), 4), np.int32)
+    kp[:, :2] = xy
+    kp[:, 2] = resp.view(np.int32)
+    kp[:, 3] = 2
+    for radius in (1, 2):
+        assert np.array_equal(lp.nms(kp, radius), orc.nms(kp, radius))
+    # ties: quantised responses force (y,x) tie-breaks
+    kq = kp.copy()
+    kq[:, 2] = np.round(resp / 1000.0).astype(np.float32).view(np.int32)
+    assert np.array_equal(lp.nms(kq, 1), orc.nms(kq, 1))
+    for n in (1, 37, 5000):
+        assert np.array_equal(lp.select_top_n(kq, n), orc.select_top_n(kq, n))
+
+
+@pytest.mark.parametrize("sigma,ch", [(1.0, 1), (2.0, 1), (1.5, 3)])
+def test_gaussian_blur(lp, orc, sigma, ch):
+    rng = np.random.default_rng(1)
+    shape = (61, 77) if ch == 1 else (61, 77, ch)
+    img = rng.uniform(0, 255, size=shape).astype(np.float32)
+    assert lp.gaussian_blur(img, sigma).tobytes() == orc.gaussian_blur(img, sigma).tobytes()
+
+
+def test_brief_descriptors(lp, orc):
+    img = orc.texture(160, 120, 2).astype(np.float32)
+    sm = orc.gaussian_blur(img, 2.0)
+    pat = orc.brief_pattern(256, 15, 42)
+    kp = np.array([[x, y, 0, 0] for x in range(15, 145, 13) for y in range(15, 105, 11)], np.int32)
+    assert np.array_equal(lp.brief_descriptors(sm, kp, pat), orc.brief_descriptors(sm, kp, pat))
+    pat512 = orc.brief_pattern(512, 15, 7)
+    assert np.array_equal(lp.brief_descriptors(sm, kp, pat512), orc.brief_descriptors(sm, kp, pat512))
+
+
+@pytest.mark.parametrize("w,h", [(640, 480), (1920, 1080)])
+def test_extract_features(lp, orc, params, w, h):
+    l, r, _ = orc.planted_pair(w, h, 0.25, 42)
+    regs = orc.partition_regions([(w, h), (w, h)], 0.25, 15)
+    pat = orc.brief_pattern(256, 15, 42)
+    for img, rg in ((l, regs[:1]), (r, regs[1:]), (l, regs)):
+        ka, da = lp.extract_features(img, rg, params.extraction, pat)
+        kb, db = orc.extract_features(img, rg, params.extraction, pat)
+        assert len(ka) == len(kb) > 0
+        assert np.array_equal(ka, kb)
+        assert np.array_equal(da, db)
+
+
+def test_extract_features_full_frame_region(lp, orc, params):
+    """A full-image region (cmd_extract, cli.hpp:172-207) with more survivors
+    than top_n in many radix buckets."""
+    img = orc.texture(800, 600, 11)
+    cfg = params.extraction
+    pat = orc.brief_pattern(cfg.n_d, cfg.patch_half, 42)
+    reg = [(15, 15, 785, 585, 0)]
+    ka, da = lp.extract_features(img, reg, cfg, pat)
+    kb, db = orc.extract_features(img, reg, cfg, pat)
+    assert np.array_equal(ka, kb) and np.array_equal(da, db)
+
+
+# ---------------------------------------------------------------- matching
+def _descs(orc, params, w=640, h=480):
+    l, r, _ = orc.planted_pair(w, h, 0.25, 42)
+    regs = orc.partition_regions([(w, h), (w, h)], 0.25, 15)
+    pat = orc.brief_pattern(256, 15, 42)
+    _, dl = orc.extract_features(l, regs[:1], params.extraction, pat)
+    _, dr = orc.extract_features(r, regs[1:], params.extraction, pat)
+    return dl, dr
+
+
+def test_match_features(lp, orc, params):
+    dl, dr = _descs(orc, params)
+    mc = params.matching
+    a = lp.match_features(dr, dl, 256, mc)
+    b = orc.match_features(dr, dl, 256, mc)
+    assert len(a) > 400 and np.array_equal(a, b)
+    # perturbed descriptors: ratio test and multi-probe paths get exercised
+    rng = np.random.default_rng(3)
+    noisy = dr.copy()
+    flips = rng.integers(0, 64, size=(len(dr), 6))
+    for i, f in enumerate(flips):
+        for b_ in f:
+            noisy[i, b_ // 64 * 0 + (b_ % 4)] ^= np.uint64(1) << np.uint64(b_)
+    for t_probes, L, k in ((16, 4, 16), (40, 6, 12), (1, 1, 20)):
+        mc2 = params.matching
+        mc2.t_probes, mc2.tables, mc2.bits = t_probes, L, k
+        a = lp.match_features(noisy, dl, 256, mc2)
+        b = orc.match_features(noisy, dl, 256, mc2)
+        assert np.array_equal(a, b), (t_probes, L, k)
+    mc2.t_probes, mc2.tables, mc2.bits = 16, 4, 16
+
+
+def test_descriptor_distances(lp, orc):
+    rng = np.random.default_rng(0)
+    a = rng.integers(0, 2**63, size=(50, 8), dtype=np.uint64)
+    b = rng.integers(0, 2**63, size=(50, 8), dtype=np.uint64)
+    assert np.array_equal(lp.descriptor_distances(a, b, 256), orc.descriptor_distances(a, b, 256))
+
+
+# ---------------------------------------------------------------- homography
+def test_dlt(lp, orc):
+    for seed in range(4):
+        src, dst, q = prosac_data(seed, n=200)
+        corr = orc.corr_array(src, dst, q)
+        for n in (4, 5, 70, 200):
+            a = lp.dlt_homography(corr[:n])
+            b = orc.dlt_homography(corr[:n])
+            assert frob_rel(a, b) < 1e-4
+            assert np.array_equal(a, b), (seed, n, frob_rel(a, b))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 7, 1234])
+def test_prosac(lp, orc, seed):
+    src, dst, q = prosac_data(seed + 3, n=300, inlier_frac=0.5, noise=1.0)
+    corr = orc.corr_array(src, dst, q)
+    for sampling in (0, 1):
+        pc = orc.default_params().prosac
+        pc.seed = seed
+        pc.sampling = sampling
+        a = lp.prosac_homography(corr, pc, trace=True)
+        b = orc.prosac_homography(corr, pc, trace=True)
+        assert a["iterations"] == b["iterations"]
+        assert np.array_equal(a["pool"], b["pool"])
+        assert np.array_equal(a["samples"], b["samples"])
+        assert frob_rel(a["model"], b["model"]) < 1e-4
+        assert np.array_equal(a["model"], b["model"])
+        assert np.array_equal(a["mask"], b["mask"]) and a["inlier_count"] == b["inlier_count"]
+
+
+def test_prosac_errors(lp, orc):
+    from paper_1810_03988_b200 import LorbError
+    pc = orc.default_params().prosac
+    few = orc.corr_array([[0, 0]] * 3, [[0, 0]] * 3, [1, 1, 1])
+    for o in (lp, orc):
+        with pytest.raises(LorbError) as e:
+            o.prosac_homography(few, pc)
+        assert e.value.name == "InsufficientMatches"
+    line = orc.corr_array([[i, 2 * i] for i in range(20)], [[i, 2 * i] for i in range(20)], [1] * 20)
+    names = []
+    for o in (lp, orc):
+        with pytest.raises(LorbError) as e:
+            o.prosac_homography(line, pc)
+        names.append(e.value.name)
+    assert names == ["NoModelFound", "NoModelFound"]
+
+
+# ---------------------------------------------------------------- compositor
+def _scene(orc):
+    l, r, th = orc.planted_pair(200, 150, 0.25, 8)
+    homs = [np.eye(3), np.array([[1, 0, th[2]], [0, 1, 0], [0, 0, 1.0]]) @ np.array(
+        [[1, 0.003, 0.6], [-0.002, 1, 0.25], [1e-5, 0, 1.0]])]
+    cv, _ = orc.compute_canvas([(200, 150), (200, 150)], homs)
+    return l, r, homs, cv
+
+
+def test_warp_seam(lp, orc):
+    l, r, homs, cv = _scene(orc)
+    for img, H in ((l, homs[0]), (r, homs[1])):
+        a = lp.warp_image(img.astype(np.float32), H, cv)
+        b = orc.warp_image(img.astype(np.float32), H, cv)
+        assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes()
+    rgb = np.random.default_rng(2).uniform(0, 255, size=(150, 200, 3)).astype(np.float32)
+    a = lp.warp_image(rgb, homs[1], cv)
+    b = orc.warp_image(rgb, homs[1], cv)
+    assert a[0].tobytes() == b[0].tobytes()
+    covs = np.stack([orc.warp_image(l.astype(np.float32), homs[0], cv)[1],
+                     orc.warp_image(r.astype(np.float32), homs[1], cv)[1]])
+    covs[0, 40:60, 30:90] = 0  # holes: several runs per row
+    assert lp.linear_seam_mask(covs).tobytes() == orc.linear_seam_mask(covs).tobytes()
+
+
+def test_pyramids(lp, orc):
+    rng = np.random.default_rng(5)
+    for w, h in ((101, 77), (64, 64), (2, 3)):
+        img = rng.uniform(0, 255, size=(h, w)).astype(np.float32)
+        if w >= 2 and h >= 2:
+            assert lp.downsample(img).tobytes() == orc.downsample(img).tobytes()
+        for tw, th in ((2 * w, 2 * h), (2 * w + 1, 2 * h - 1)):
+            assert lp.upsample(img, tw, th).tobytes() == orc.upsample(img, tw, th).tobytes()
+    img = rng.uniform(0, 255, size=(77, 101)).astype(np.float32)
+    for L in (1, 3, 5):
+        for f in ("gaussian_pyramid", "build_laplacian"):
+            a, b = getattr(lp, f)(img, L), getattr(orc, f)(img, L)
+            assert all(x.tobytes() == y.tobytes() for x, y in zip(a, b)), (f, L)
+        lap = orc.build_laplacian(img, L)
+        assert lp.collapse_laplacian(lap).tobytes() == orc.collapse_laplacian(lap).tobytes()
+
+
+@pytest.mark.parametrize("levels", [1, 3, 4])
+def test_multiband_blend(lp, orc, levels):
+    l, r, homs, cv = _scene(orc)
+    w0, c0 = orc.warp_image(l.astype(np.float32), homs[0], cv)
+    w1, c1 = orc.warp_image(r.astype(np.float32), homs[1], cv)
+    masks = orc.linear_seam_mask(np.stack([c0, c1]))
+    imgs = np.stack([w0, w1])
+    assert np.array_equal(lp.multiband_blend(imgs, masks, levels), orc.multiband_blend(imgs, masks, levels))
+
+
+# ---------------------------------------------------------------- whole frames
+def _assert_frame_equal(a, b):
+    assert a["canvas"] == b["canvas"]
+    for c in range(len(a["keypoints"])):
+        assert np.array_equal(a["keypoints"][c], b["keypoints"][c]), c
+        assert np.array_equal(a["descriptors"][c], b["descriptors"][c]), c
+    for p in range(len(a["matches"])):
+        assert np.array_equal(a["matches"][p], b["matches"][p]), p
+    assert np.array_equal(a["homographies"], b["homographies"])
+    assert np.array_equal(a["panorama"], b["panorama"])
+
+
+def test_stitch_frame_cfg1(lp, orc, params):
+    """BASELINE config 1: two 640x480 planted frames, L-ORB + LSH + PROSAC + blend."""
+    l, r, th = orc.planted_pair(640, 480, 0.25, 42)
+    a = lp.stitch_frame([l, r], params, frame_index=0)
+    b = orc.stitch_frame([l, r], params, frame_index=0)
+    _assert_frame_equal(a, b)
+    assert abs(a["homographies"][1][0, 2] - th[2]) < 1e-6
+
+
+def test_stitch_sequence_cfg2_small(lp, orc, params):
+    """Config 2 style: sequence frames with a moving square, per-frame re-registration."""
+    for t in (0, 5, 31):
+        l, r = orc.sequence_frame(480, 270, t, 0.25, 42)
+        _assert_frame_equal(lp.stitch_frame([l, r], params, frame_index=t),
+                            orc.stitch_frame([l, r], params, frame_index=t))
+
+
+def test_stitch_chain_4cam_small(lp, orc, params):
+    """Config 3/4 style chain (smaller frames): 4 cameras, 6 regions, 3 pairs."""
+    cams, wide, shift = chain_cameras(orc, 4, 400, 240)
+    _assert_frame_equal(lp.stitch_frame(cams, params, frame_index=2),
+                        orc.stitch_frame(cams, params, frame_index=2))
+
+
+def test_rig_cache_and_device_inputs(lp, orc, params):
+    """HomographyCache semantics (pipeline.hpp:259-286) and device-resident inputs."""
+    import torch
+    from paper_1810_03988_b200 import Rig
+    p = orc.default_params()
+    p.seed = p.matching.seed = 42
+    p.homography_refresh = 3
+    l, r, _ = orc.planted_pair(320, 240, 0.25, 42)
+    rig = Rig(lp, 2, 320, 240, p)
+    outs = [rig.stitch([l, r], t) for t in range(4)]
+    assert [o["estimated"] for o in outs] == [True, False, False, True]
+    want = orc.stitch_frame([l, r], p, frame_index=0)
+    assert np.array_equal(outs[1]["panorama"], want["panorama"])
+    dev = [torch.from_numpy(l).cuda(), torch.from_numpy(r).cuda()]
+    o = rig.stitch(dev, 4)
+    assert np.array_equal(o["panorama"], want["panorama"])
+
+
+def test_full_size_4k_4cam(lp, orc, params):
+    """Config 3 at full size (4 cameras x 3840x2160, canvas ~12480x2160): the
+    whole frame bit-exact against the oracle, plus size-independent
+    properties: every chained homography is the planted shift (frobenius_rel
+    < 1e-4) and the panorama reproduces the wide texture to +-1 LSB on >= 99%
+    of the covered canvas."""
+    cams, wide, shift = chain_cameras(orc, 4, 3840, 2160)
+    from paper_1810_03988_b200 import Rig
+    rig = Rig(lp, 4, 3840, 2160, params)
+    out = rig.stitch(cams, 0, details=True)
+    H = out["homographies"]
+    for c in range(4):
+        want = np.array([[1, 0, c * shift], [0, 1, 0], [0, 0, 1.0]])
+        assert frob_rel(H[c], want) < 1e-4
+    W, Hh, ox, oy = out["canvas"]
+    sub = out["panorama"][-oy:-oy + 2160, -ox:-ox + wide.shape[1]].astype(int)
+    assert (np.abs(sub - wide.astype(int)) <= 1).mean() >= 0.99
+    assert [len(k) for k in out["keypoints"]] == [500, 1000, 1000, 500]
+    ref_frame = orc.stitch_frame(cams, params, frame_index=0)
+    _assert_frame_equal(out, ref_frame)
+
+
+def test_errors_match_oracle(lp, orc):
+    from paper_1810_03988_b200 import LorbError
+    img = rand_image(32, 32, 1)
+    calls = [
+        lambda o: o.fast_corners(img, (0, 0, 3, 3, 0)),
+        lambda o: o.harris_response(img, np.array([[2, 2]])),
+        lambda o: o.upsample(np.zeros((4, 4), np.float32), 12, 8),
+        lambda o: o.gaussian_pyramid(np.zeros((4, 4), np.float32), 5),
+        lambda o: o.downsample(np.zeros((1, 4), np.float32)),
+        lambda o: o.match_features(np.zeros((0, 8), np.uint64), np.zeros((3, 8), np.uint64), 256,
+                                   o.default_params().matching),
+        lambda o: o.dlt_homography(o.corr_array([[0, 0], [1, 1], [2, 2], [0, 5]],
+                                                [[0, 0], [1, 1], [2, 2], [0, 5]], [1] * 4)),
+    ]
+    for f in calls:
+        names = []
+        for o in (lp, orc):
+            with pytest.raises(LorbError) as e:
+                f(o)
+            names.append(e.value.name)
+        assert names[0] == names[1], names
