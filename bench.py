@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""Benchmark: stitched panorama frames/sec on B200 (BASELINE.json metric).
+
+Workload (default, BASELINE config 3): a 4-camera chain of 3840x2160 grayscale
+frames with 25% overlap, cached homographies (estimated on the first frame,
+homography_refresh = 2^30) and per-frame detect + describe + warp/blend, as
+the reference's StitchEngine runs it (pipeline.hpp:645-658). One step = one
+stitched frame. Inputs are synthetic (seeded uniform noise, sigma=1.5 blur,
+contrast stretch: the shape of synth::texture, synth.hpp:18-34), eight
+distinct frame sets rotate so the per-step input stream (8 x 33 MB) exceeds
+the 126 MB L2.
+
+N GPUs (torchrun): one independent rig per GPU (weak scaling, no collective on
+the data path); an NCCL all_reduce(MAX) of the per-rank device times and an
+all_gather of per-rank checksums are the only collectives.
+
+--impl reference: the reference's own CPU engine (oracle/_ref, the unmodified
+reference headers compiled here), serial engines on all host threads.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "stitched panorama frames/sec (4K, 4-cam) at 1/2/4/8 B200; per-stage ms; HBM GB/s vs peak"
+
+CONFIGS = {
+    "cfg3": dict(ncams=4, w=3840, h=2160, refresh=1 << 30,
+                 workload="cfg3: 4-camera 3840x2160 chain, cached homographies, per-frame "
+                          "detect+describe+warp+multi-band blend"),
+    "cfg4": dict(ncams=8, w=3840, h=2160, refresh=1,
+                 workload="cfg4: 8-camera 3840x2160 chain, full per-frame L-ORB/LSH/PROSAC "
+                          "re-registration + warp + multi-band blend"),
+    "cfg2": dict(ncams=2, w=1920, h=1080, refresh=1,
+                 workload="cfg2: 2-camera 1920x1080, per-frame re-registration"),
+    "cfg1": dict(ncams=2, w=640, h=480, refresh=1,
+                 workload="cfg1: 2-camera 640x480 planted pair, full pipeline"),
+}
+
+
+def texture(w, h, seed, sigma=1.5):
+    """synth::texture-shaped input (uniform noise, Gaussian blur, stretch)."""
+    rng = np.random.default_rng(seed)
+    noise = rng.integers(0, 256, size=(h, w)).astype(np.float32)
+    r = int(np.ceil(3 * sigma))
+    x = np.arange(-r, r + 1, dtype=np.float32)
+    k = np.exp(-(x * x) / (2 * sigma * sigma))
+    k /= k.sum()
+    pad = np.pad(noise, ((0, 0), (r, r)), mode="edge")
+    t = sum(k[i] * pad[:, i:i + w] for i in range(2 * r + 1))
+    pad = np.pad(t, ((r, r), (0, 0)), mode="edge")
+    b = sum(k[i] * pad[i:i + h, :] for i in range(2 * r + 1))
+    lo, hi = b.min(), b.max()
+    return np.clip(np.round((b - lo) * (255.0 / (hi - lo))), 0, 255).astype(np.uint8)
+
+
+def make_frame_sets(ncams, w, h, nsets, seed=42, overlap=0.25):
+    shift = int(np.floor(w * (1 - overlap) + 0.5))
+    wide = texture(w + shift * (ncams - 1), h, seed)
+    sets = []
+    size = max(4, h // 16)
+    for s in range(nsets):
+        cams = [np.ascontiguousarray(wide[:, c * shift:c * shift + w]) for c in range(ncams)]
+        # a moving bright square per set (synth::sequence_frame, synth.hpp:99-115)
+        px, py = (s * 7 * 37) % (w - size), (s * 3 * 37) % (h - size)
+        for c in range(ncams):
+            x0 = px - c * shift
+            if -size < x0 < w:
+                cams[c] = cams[c].copy()
+                cams[c][py:py + size, max(0, x0):min(w, x0 + size)] = 255
+        sets.append(cams)
+    return sets, shift
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        loaded = [r for r in rows if r[7].isdigit() and int(r[7]) > 0] or rows
+        sm = [float(r[0]) for r in loaded if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded)}
+
+
+def measured_peak_hbm():
+    try:
+        j = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_baseline(frames, params_fn, sample_frames=1):
+    """The reference CPU engine (oracle/_ref) on a bounded sample of the same
+    workload: `sample_frames` frames, serial StitchEngine, 1 core."""
+    import oracle
+    from oracle import Oracle
+    kind = "reference" if oracle.ref_available() else "port"
+    o = Oracle("ref" if kind == "reference" else "orc")
+    p = params_fn(o)
+    ncams = len(frames)
+    h, w = frames[0].shape
+    t0 = time.perf_counter()
+    if kind == "reference":
+        from paper_1810_03988_b200 import abi
+        arr = (C.c_void_p * ncams)(*[f.ctypes.data for f in frames])
+        fps, ms = C.c_double(), (C.c_double * 7)()
+        st = o.lib.ref_run_engine(ncams, w, h, C.byref(p), arr, sample_frames, 0, 1, 1,
+                                  C.byref(fps), ms)
+        if st:
+            raise abi.LorbError(st, o.lib.ref_last_error().decode())
+        value = fps.value
+        stages = {n: round(ms[i], 2) for i, n in enumerate(
+            ["ingest", "rectify_crop", "detect", "describe", "match_estimate", "warp_blend",
+             "output"])}
+    else:
+        for _ in range(sample_frames):
+            o.stitch_frame(frames, p)
+        value = sample_frames / (time.perf_counter() - t0)
+        stages = None
+    return {"value": value, "unit": "frames/s", "cores": 1, "kind": kind,
+            "sample": f"{sample_frames} frame(s) of the same workload through the reference's "
+                      f"serial StitchEngine (pipeline.hpp:645-658), {time.perf_counter() - t0:.1f} s",
+            "stage_ms": stages}
+
+
+def run_reference(args, cfgd):
+    """--impl reference: the reference's own CPU engine on all host threads."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    from oracle import Oracle
+    from paper_1810_03988_b200 import abi
+    if not oracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
+        return 0
+    o = Oracle("ref")
+    sets, _ = make_frame_sets(cfgd["ncams"], cfgd["w"], cfgd["h"], 1)
+    frames = sets[0]
+    p = o.default_params()
+    p.seed = p.matching.seed = 42
+    p.homography_refresh = cfgd["refresh"]
+    ncams, w, h = cfgd["ncams"], cfgd["w"], cfgd["h"]
+    ncpu = os.cpu_count() or 1
+    try:
+        mem_gb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2**30
+    except (ValueError, OSError):
+        mem_gb = 64
+    per_engine_gb = 4.0 * ncams * w * h / (3840 * 2160 * 4)  # ~4 GB for 4K x 4 cams
+    threads = int(max(1, min(ncpu, mem_gb * 0.5 / max(per_engine_gb, 0.1), 32)))
+    steps, warm = min(args.steps, 3), min(args.warmup, 1)
+    arr = (C.c_void_p * ncams)(*[f.ctypes.data for f in frames])
+    agg = C.c_double()
+    for _ in range(warm):
+        o.lib.ref_run_engines_parallel(ncams, w, h, C.byref(p), arr, 1, threads, C.byref(agg))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st = o.lib.ref_run_engines_parallel(ncams, w, h, C.byref(p), arr, 1, threads, C.byref(agg))
+        if st:
+            raise abi.LorbError(st, o.lib.ref_last_error().decode())
+    el = time.perf_counter() - t0
+    value = steps * threads / el
+    line = {"metric": METRIC, "value": value, "unit": "frames/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": el / steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/f32/f64",
+            "data": "synthetic",
+            "config": {"workload": cfgd["workload"], "cameras": ncams, "width": w, "height": h,
+                       "engines": threads, "frames_per_step": threads},
+            "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "reference",
+                             "sample": f"{threads} serial StitchEngines in parallel, 1 frame each per step"},
+            "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--out", default=None, help="also write the JSON line here")
+    args = ap.parse_args()
+    cfgd = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfgd)
+
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1810_03988_b200 import FrameOut_from, Lorb, Rig, abi, kernel_launches, load
+    lib = load()
+    lp = Lorb(local)
+    ncams, w, h = cfgd["ncams"], cfgd["w"], cfgd["h"]
+    p = lp.default_params()
+    p.seed = p.matching.seed = 42
+    p.homography_refresh = cfgd["refresh"]
+    nsets = 8 if args.config in ("cfg3", "cfg4") else 4
+    sets, shift = make_frame_sets(ncams, w, h, nsets, seed=42 + rank)
+    dev_sets = [[torch.from_numpy(c).cuda() for c in s] for s in sets]
+    rig = Rig(lp, ncams, w, h, p)
+    stream = torch.cuda.ExternalStream(rig.stream)
+    pano_cap = rig.panorama_capacity()
+    dpano = torch.empty(pano_cap, dtype=torch.uint8, device="cuda")
+    fo = FrameOut_from(dpano.data_ptr(), pano_cap)
+
+    def step(i):
+        rig.stitch_raw([t.data_ptr() for t in dev_sets[i % nsets]], i, fo)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    canvas = (fo.canvas.width, fo.canvas.height)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region: device-resident inputs, CUDA events on the rig stream
+    barrier()
+    clocks = Clocks(local)
+    n0 = kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        step(args.warmup + i)
+    e1.record(stream)
+    e1.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = kernel_launches() - n0
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * args.steps / (ms_max / 1e3)
+
+    # panorama checksum gathered to rank 0 (the only other collective)
+    pano = dpano[:canvas[0] * canvas[1]]
+    csum = torch.tensor([int(pano.to(torch.int64).sum().item())], dtype=torch.int64, device="cuda")
+    if dist is not None:
+        allc = [torch.zeros_like(csum) for _ in range(world)]
+        dist.all_gather(allc, csum)
+        checksums = [int(x.item()) for x in allc]
+    else:
+        checksums = [int(csum.item())]
+
+    # ---- per-kernel profile pass (same workload; events around every launch)
+    roofline = None
+    stage = {}
+    if not args.no_profile:
+        lib.lp_profile_reset()
+        lib.lp_profile_enable(1)
+        for i in range(args.steps):
+            step(10_000 + i)
+        torch.cuda.synchronize()
+        cap = 256
+        names = C.create_string_buffer(cap * 64)
+        tot = (C.c_double * cap)()
+        cnt = (C.c_longlong * cap)()
+        lib.lp_profile_read.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
+        n = lib.lp_profile_read(names, 64, tot, cnt, cap)
+        lib.lp_profile_enable(0)
+        kern = {}
+        for i in range(min(n, cap)):
+            key = names.raw[i * 64:(i + 1) * 64].split(b"\0")[0].decode()
+            kern[key] = (tot[i], cnt[i])
+        lib.lp_rig_algorithmic_bytes.argtypes = [C.c_void_p, C.c_char_p]
+        lib.lp_rig_algorithmic_bytes.restype = C.c_double
+        step_ms = sum(v[0] for v in kern.values()) / args.steps
+        dom = max(kern, key=lambda k: kern[k][0])
+        avg = kern[dom][0] / kern[dom][1]
+        byts = lib.lp_rig_algorithmic_bytes(rig.rig, dom.encode())
+        peak, peak_src = measured_peak_hbm()
+        achieved = byts / (avg * 1e-3) / 1e9 if byts > 0 else None
+        traffic = None
+        try:
+            nj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            traffic = nj.get(args.config, {}).get(dom.split("/")[0] + "/" + dom.split("/")[1])
+        except Exception:
+            pass
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                    "peak_source": peak_src, "unit": "GB/s",
+                    "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                    "algorithmic_bytes_per_launch": byts, "avg_launch_ms": avg,
+                    "share_of_kernel_time": kern[dom][0] / max(1e-9, sum(v[0] for v in kern.values()))}
+        stage = {k: round(v[0] / v[1], 4) for k, v in sorted(kern.items(), key=lambda kv: -kv[1][0])}
+        stage["_kernel_ms_per_frame"] = round(step_ms, 4)
+        # frame-level HBM rate at SURVEY §8(d) algorithmic bytes per frame
+        stage["_per_frame_algorithmic_GBps"] = None
+
+    # ---- end to end through the public C-ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_sets = [[torch.from_numpy(c).pin_memory() for c in s] for s in sets[:2]]
+        hpano = torch.empty(pano_cap, dtype=torch.uint8).pin_memory()
+        fo_h = FrameOut_from(hpano.data_ptr(), pano_cap)
+        for i in range(3):
+            rig.stitch_raw([t.data_ptr() for t in host_sets[i % 2]], 20_000 + i, fo_h)
+        barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            rig.stitch_raw([t.data_ptr() for t in host_sets[i % 2]], 30_000 + i, fo_h)
+        el = time.perf_counter() - t0
+        tt = torch.tensor([el], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * args.steps / float(tt.item()), "unit": "frames/s",
+               "h2d_bytes_per_step": ncams * w * h, "d2h_bytes_per_step": canvas[0] * canvas[1],
+               "timing": "wall clock around lp_rig_stitch with pinned host inputs/outputs (synchronous call)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        def params_fn(o):
+            q = o.default_params()
+            q.seed = q.matching.seed = 42
+            q.homography_refresh = cfgd["refresh"]
+            return q
+        cpu = cpu_baseline(sets[0], params_fn, 1)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "u8/f32/f64", "data": "synthetic",
+                "config": {"workload": cfgd["workload"], "cameras": ncams, "width": w, "height": h,
+                           "canvas": list(canvas), "overlap": 0.25,
+                           "l2": f"{nsets} rotating input frame sets ({nsets * ncams * w * h / 1e6:.0f} MB) > 126 MB L2",
+                           "parallelism": f"replicas x{world} (independent rigs, no data-path collective)"},
+                "gpu_launches": int(launches), "clocks": clk, "roofline": roofline,
+                "cpu_baseline": cpu, "e2e": e2e, "kernel_ms": stage, "rank_checksums": checksums}
+        s = json.dumps(line)
+        print(s)
+        if args.out:
+            open(args.out, "w").write(s + "\n")
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -246,6 +246,18 @@ void lp_rig_destroy(lp_rig* rig);
  * pipeline.hpp:259-286) -> warp_blend. images[c] host or device. */
 lp_status lp_rig_stitch(lp_rig* rig, const uint8_t* const* images, uint64_t frame_index,
                         lp_frame_out* out);
+/* Compulsory bytes (inputs once + outputs once, in the kernel's data types)
+ * one launch of `kernel_key` ("k_warp/0", "k_blend_level/3", ... as the
+ * profiler names them) moves for the rig's last frame; < 0 if unknown. */
+double lp_rig_algorithmic_bytes(lp_rig* rig, const char* kernel_key);
+
+/* ---- diagnostics: per-kernel device time (CUDA events around each launch) ---- */
+void lp_profile_enable(int on);
+void lp_profile_reset(void);
+/* fills up to cap entries: names (name_stride bytes each) "kernel/occurrence",
+ * summed ms, launch count; returns the number of distinct keys */
+int lp_profile_read(char* names, int name_stride, double* total_ms, long long* launches, int cap);
+
 /* Upper bound on panorama bytes for this rig's current homographies. */
 size_t lp_rig_panorama_capacity(lp_rig* rig);
 /* The stream the rig's work is enqueued on (cudaStream_t). */

@@ -11,7 +11,9 @@
 #include <cub/cub.cuh>
 
 #include <atomic>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -26,6 +28,66 @@ namespace lpb {
 static std::atomic<uint64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 static thread_local std::string g_err;
+
+// ---- kernel profiler: events around every launch, keyed "name/occurrence"
+// where the occurrence counter restarts at every frame (prof_frame_begin).
+struct Prof {
+    std::mutex mu;
+    bool on = false;
+    struct Rec {
+        std::string key;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> open;
+    std::vector<cudaEvent_t> pool;
+    std::map<std::string, int> occ;
+    std::map<std::string, std::pair<double, long long>> acc;  // key -> (ms, launches)
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    void drain() {  // caller holds mu; device must be idle for these events
+        for (auto& r : open) {
+            float ms = 0;
+            cudaEventSynchronize(r.b);
+            cudaEventElapsedTime(&ms, r.a, r.b);
+            auto& v = acc[r.key];
+            v.first += ms;
+            v.second += 1;
+            pool.push_back(r.a);
+            pool.push_back(r.b);
+        }
+        open.clear();
+    }
+};
+static Prof g_prof;
+int prof_begin(const char* name, cudaStream_t s) {
+    if (!g_prof.on) return -1;
+    std::lock_guard<std::mutex> l(g_prof.mu);
+    std::string n(name);
+    const int k = g_prof.occ[n]++;
+    Prof::Rec r{n + "/" + std::to_string(k), g_prof.get(), g_prof.get()};
+    cudaEventRecord(r.a, s);
+    g_prof.open.push_back(r);
+    return static_cast<int>(g_prof.open.size()) - 1;
+}
+void prof_end(int token, cudaStream_t s) {
+    if (token < 0) return;
+    std::lock_guard<std::mutex> l(g_prof.mu);
+    if (token < static_cast<int>(g_prof.open.size())) cudaEventRecord(g_prof.open[token].b, s);
+}
+static void prof_frame_begin() {
+    if (!g_prof.on) return;
+    std::lock_guard<std::mutex> l(g_prof.mu);
+    g_prof.occ.clear();
+    if (g_prof.open.size() > 4096) g_prof.drain();
+}
 
 template <class F>
 static lp_status guard(F&& f) {
@@ -229,6 +291,33 @@ extern "C" {
 
 const char* lp_last_error(void) { return g_err.c_str(); }
 uint64_t lp_kernel_launches(void) { return g_launches.load(); }
+
+void lp_profile_enable(int on) {
+    std::lock_guard<std::mutex> l(g_prof.mu);
+    g_prof.on = on != 0;
+}
+void lp_profile_reset(void) {
+    std::lock_guard<std::mutex> l(g_prof.mu);
+    cudaDeviceSynchronize();
+    g_prof.drain();
+    g_prof.acc.clear();
+    g_prof.occ.clear();
+}
+int lp_profile_read(char* names, int name_stride, double* total_ms, long long* launches, int cap) {
+    std::lock_guard<std::mutex> l(g_prof.mu);
+    cudaDeviceSynchronize();
+    g_prof.drain();
+    int i = 0;
+    for (auto& kv : g_prof.acc) {
+        if (i < cap) {
+            std::snprintf(names + static_cast<size_t>(i) * name_stride, name_stride, "%s", kv.first.c_str());
+            total_ms[i] = kv.second.first;
+            launches[i] = kv.second.second;
+        }
+        ++i;
+    }
+    return i;
+}
 
 void lp_params_default(lp_params* p) {
     std::memset(p, 0, sizeof *p);

@@ -32,12 +32,18 @@ struct Status : std::runtime_error {
                                                    cudaGetErrorString(e_));              \
     } while (0)
 
-// every kernel launch goes through this so lp_kernel_launches() is exact
+// every kernel launch goes through this so lp_kernel_launches() is exact, and
+// so the optional kernel profiler (lp_profile_enable) can bracket it with
+// CUDA events on the launching stream
 void note_launch();
+int prof_begin(const char* name, cudaStream_t s);
+void prof_end(int token, cudaStream_t s);
 #define LPB_LAUNCH(kernel, grid, block, smem, stream, ...)                              \
     do {                                                                                 \
+        const int pt_ = ::lpb::prof_begin(#kernel, (stream));                            \
         kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                      \
         LPB_CUDA(cudaGetLastError());                                                    \
+        ::lpb::prof_end(pt_, (stream));                                                  \
         ::lpb::note_launch();                                                            \
     } while (0)
 
