@@ -237,7 +237,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    from paper_1810_03988_b200 import FrameOut_from, Lorb, Rig, abi, kernel_launches, load
+    from paper_1810_03988_b200 import Lorb, Rig, abi, frame_out, kernel_launches, load
     lib = load()
     lp = Lorb(local)
     ncams, w, h = cfgd["ncams"], cfgd["w"], cfgd["h"]
@@ -251,7 +251,7 @@ def main():
     stream = torch.cuda.ExternalStream(rig.stream)
     pano_cap = rig.panorama_capacity()
     dpano = torch.empty(pano_cap, dtype=torch.uint8, device="cuda")
-    fo = FrameOut_from(dpano.data_ptr(), pano_cap)
+    fo = frame_out(dpano.data_ptr(), pano_cap)
 
     def step(i):
         rig.stitch_raw([t.data_ptr() for t in dev_sets[i % nsets]], i, fo)
@@ -345,7 +345,7 @@ def main():
     if not args.no_e2e:
         host_sets = [[torch.from_numpy(c).pin_memory() for c in s] for s in sets[:2]]
         hpano = torch.empty(pano_cap, dtype=torch.uint8).pin_memory()
-        fo_h = FrameOut_from(hpano.data_ptr(), pano_cap)
+        fo_h = frame_out(hpano.data_ptr(), pano_cap)
         for i in range(3):
             rig.stitch_raw([t.data_ptr() for t in host_sets[i % 2]], 20_000 + i, fo_h)
         barrier()

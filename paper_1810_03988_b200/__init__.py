@@ -9,4 +9,5 @@ the C-ABI in include/lorbpano_b200.h.
     out = rig.stitch([cam0, cam1])     # panorama + homographies
 """
 from .abi import LorbError  # noqa: F401
-from .lib import Lorb, Rig, build, kernel_launches, load  # noqa: F401
+from .lib import Lorb, Rig, build, frame_out, kernel_launches, load  # noqa: F401
+from . import abi  # noqa: F401

@@ -68,6 +68,15 @@ def kernel_launches():
     return int(load().lp_kernel_launches())
 
 
+def frame_out(pano_ptr, pano_cap):
+    """A FrameOut that only receives the panorama (host or device address):
+    with a device address lp_rig_stitch returns without synchronising."""
+    fo = abi.FrameOut()
+    fo.panorama = C.cast(C.c_void_p(pano_ptr), abi.c_u8p)
+    fo.pano_cap = pano_cap
+    return fo
+
+
 def _check(lib, st):
     if st != 0:
         raise abi.LorbError(st, lib.lp_last_error().decode())
