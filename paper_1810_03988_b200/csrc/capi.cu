@@ -966,12 +966,19 @@ namespace lpb {
 struct ComposeBuffers {
     int ncams = 0, levels = 0;
     std::vector<Win> win;  // host copy
-    DBuf d_win, d_G, d_M, d_cov, d_R, d_src, d_hinv, taps;
+    std::vector<Win> win_unused_;
     std::vector<std::unique_ptr<DBuf>> bufs;
     ComposeArgs args{};
 
-    void build(int ncams_, int levels_, int W0, int H0, const std::vector<Win>& win0, bool with_cov,
+    DBuf runs, runs_used, status;
+    std::vector<float*> host_G, host_M;  // [c * levels + k]
+
+    // analytic: level-0 masks come from coverage runs (the rig); otherwise the
+    // caller fills M[c][0] (lp_multiband_blend).
+    void build(int ncams_, int levels_, int W0, int H0, const std::vector<Win>& win0, bool analytic,
                cudaStream_t s) {
+        if (ncams_ > kMaxCompCams) throw Status(LP_BAD_PARAMS, "compositor: too many cameras");
+        if (levels_ > kMaxCompLevels) throw Status(LP_TOO_MANY_LEVELS, "compositor: too many blend levels");
         ncams = ncams_;
         levels = levels_;
         bufs.clear();
@@ -979,6 +986,7 @@ struct ComposeBuffers {
         args = ComposeArgs{};
         args.ncams = ncams;
         args.levels = levels;
+        args.analytic_masks = analytic ? 1 : 0;
         int W = W0, H = H0;
         for (int k = 0; k < levels; ++k) {
             args.W[k] = W;
@@ -986,8 +994,13 @@ struct ComposeBuffers {
             W /= 2;
             H /= 2;
         }
-        std::vector<float*> G(static_cast<size_t>(ncams) * levels), M(G.size());
-        std::vector<uint8_t*> cov(ncams, nullptr);
+        host_G.assign(static_cast<size_t>(ncams) * levels, nullptr);
+        host_M.assign(host_G.size(), nullptr);
+        auto alloc = [&](size_t bytes) {
+            bufs.push_back(std::make_unique<DBuf>(std::max<size_t>(bytes, 16), s));
+            return bufs.back()->p;
+        };
+        size_t total_rows = 0;
         for (int c = 0; c < ncams; ++c) {
             const Win w0 = win0[c];
             for (int k = 0; k < levels; ++k) {
@@ -999,39 +1012,36 @@ struct ComposeBuffers {
                 w.w = std::max(0, x1 - w.x0);
                 w.h = std::max(0, y1 - w.y0);
                 win[c * levels + k] = w;
+                args.win[c][k] = w;
                 const size_t np = static_cast<size_t>(w.w) * w.h;
-                bufs.push_back(std::make_unique<DBuf>(sizeof(float) * std::max<size_t>(np, 1), s));
-                G[c * levels + k] = bufs.back()->as<float>();
-                bufs.push_back(std::make_unique<DBuf>(sizeof(float) * std::max<size_t>(np, 1), s));
-                M[c * levels + k] = bufs.back()->as<float>();
+                args.G[c][k] = static_cast<float*>(alloc(sizeof(float) * np));
+                if (k > 0 || !analytic) args.M[c][k] = static_cast<float*>(alloc(sizeof(float) * np));
+                host_G[c * levels + k] = args.G[c][k];
+                host_M[c * levels + k] = args.M[c][k];
             }
-            if (with_cov) {
+            if (analytic) {
                 const Win w = win[c * levels];
-                bufs.push_back(std::make_unique<DBuf>(std::max<size_t>(static_cast<size_t>(w.w) * w.h, 1), s));
-                cov[c] = bufs.back()->as<uint8_t>();
+                args.cov_words[c] = cdiv(w.w, 32);
+                args.cov[c] = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * args.cov_words[c] * std::max(w.h, 1)));
+                args.run_rows[c] = static_cast<int2*>(alloc(sizeof(int2) * std::max(w.h, 1)));
+                total_rows += w.h;
             }
         }
-        std::vector<float*> R(levels, nullptr);
-        for (int k = 1; k < levels; ++k) {
-            bufs.push_back(std::make_unique<DBuf>(sizeof(float) * std::max<size_t>(static_cast<size_t>(args.W[k]) * args.H[k], 1), s));
-            R[k] = bufs.back()->as<float>();
+        for (int k = 1; k < levels; ++k)
+            args.R[k] = static_cast<float*>(alloc(sizeof(float) * static_cast<size_t>(args.W[k]) * args.H[k]));
+        if (analytic) {
+            args.runs_cap = static_cast<int>(std::min<size_t>(total_rows * 8 + 4096, 1u << 30));
+            runs = DBuf(sizeof(int2) * args.runs_cap, s);
+            runs_used = DBuf(sizeof(int), s);
+            args.runs = runs.as<int2>();
+            args.runs_used = runs_used.as<int>();
         }
-        d_win = upload(win, s);
-        d_G = upload(G, s);
-        d_M = upload(M, s);
-        d_cov = upload(cov, s);
-        d_R = upload(R, s);
-        taps = upload(host::gaussian_kernel(1.0f), s);
-        args.win = d_win.as<Win>();
-        args.G = d_G.as<float* const>();
-        args.M = d_M.as<float* const>();
-        args.cov = d_cov.as<uint8_t* const>();
-        args.R = d_R.as<float* const>();
-        args.down_taps = taps.as<float>();
-        host_G = G;
-        host_M = M;
+        status = DBuf(sizeof(int), s);
+        LPB_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int), s));
+        args.status = status.as<int>();
+        auto taps = host::gaussian_kernel(1.0f);
+        for (int q = 0; q < 7; ++q) args.down_taps[q] = taps[q];
     }
-    std::vector<float*> host_G, host_M;
 };
 
 static void check_levels(int w, int h, int levels) {  // gaussian_pyramid, imgops.hpp:143-150
@@ -1079,7 +1089,7 @@ extern "C" lp_status lp_multiband_blend(lp_ctx* ctx, const float* images, const 
                     LPB_LAUNCH(k_deinterleave, cdiv(np, 256), 256, 0, s, di.d + np * ch * c, static_cast<int>(np), ch,
                                cc, cb.host_G[c * levels]);
             }
-            blend_launch(cb.args, cb.win.data(), s);
+            blend_launch(cb.args, s);
             if (ch == 1)
                 LPB_CUDA(cudaMemcpyAsync(dout.d, o1.p, np, cudaMemcpyDeviceToDevice, s));
             else

@@ -3,26 +3,31 @@
 // The reference materialises, per camera, full-canvas float rasters for the
 // warp, coverage, seam mask, Laplacian pyramid and mask pyramid
 // (compose.hpp:72-215). Here every camera only owns a window of the canvas:
-// its coverage bounding box dilated by the pyramid support (>= 4*2^L+8 px at
+// its coverage bounding box dilated by the pyramid support (4*2^L+8 px at
 // level 0) and aligned to 2^(L-1). Outside its window a camera's warped
 // image, mask, Gaussian levels and Laplacian bands are exactly zero in the
 // reference, and a zero-weight term adds +-0 to a +0-seeded accumulator, so
 // skipping it leaves every accumulator bit-identical.
 //
-// Kernels per frame (L levels):
-//   k_warp        FP64 inverse map + bilinear (compose.hpp:72-95) -> G0, cov
-//   k_seam_rows   per row, warp-ballot run lengths -> min(forward, backward)
-//                 distance (compose.hpp:108-120)
-//   k_seam_norm   per pixel camera-ordered sum and division (123-129)
-//   k_pyr_down    (L-1)x: shared-memory tile, 7-tap σ=1 blur evaluated only
-//                 at the kept even samples (imgops.hpp:106-116), image and
-//                 mask pyramids in one pass
-//   k_blend_level Lx, top to bottom: the band of every camera
-//                 (G_k - upsample(G_k+1), compose.hpp:134-147) weighted by
-//                 its mask level and accumulated in camera order (182-192),
-//                 renormalised (196-202), and collapsed with the upsampled
-//                 coarser result (149-158); level 0 writes the u8 panorama
-//                 with to_u8 where any camera covers (206-213).
+// Per frame (L levels), all geometry in the constant bank (ComposeArgs):
+//   k_warp        FP64 inverse map + bilinear (compose.hpp:72-95) -> G0 window
+//                 and one coverage bit per pixel (warp ballot per 32 px)
+//   k_runs        warp per window row: covered runs [start,end) from the bit
+//                 words (start/end masks + warp prefix sums). The linear seam
+//                 mask (compose.hpp:101-131) is then analytic: distance to the
+//                 run ends, min(fwd, bwd), divided by the camera-ordered sum —
+//                 never materialised at level 0
+//   k_pyr_down    (L-1)x: shared-memory tile; 7-tap σ=1 blur evaluated only at
+//                 the kept even samples (imgops.hpp:106-116); image and mask
+//                 pyramids in one pass (level-0 mask computed from the runs)
+//   k_blend_level Lx, top to bottom: 64x16 tile per CTA; the CTA culls cameras
+//                 whose window misses the tile, stages the coarser level of
+//                 each remaining camera and the coarser collapse result in
+//                 shared memory, and per pixel accumulates the bands
+//                 (G_k - upsample(G_k+1), compose.hpp:134-147) x mask level in
+//                 camera order (182-192), renormalises (196-202), adds the
+//                 upsampled coarser result (149-158); level 0 writes the u8
+//                 panorama with to_u8 where any camera covers (206-213).
 // Accumulation orders are the reference's; FP ops are round-to-nearest, no FMA.
 #include "compose.cuh"
 
@@ -31,155 +36,12 @@ namespace lpb {
 __device__ __forceinline__ bool in_win(const Win& w, int x, int y) {
     return x >= w.x0 && x < w.x0 + w.w && y >= w.y0 && y < w.y0 + w.h;
 }
-// value of a windowed buffer at canvas-level coordinates (zero outside)
 __device__ __forceinline__ float win_at(const float* buf, const Win& w, int x, int y) {
     return in_win(w, x, y) ? buf[static_cast<size_t>(y - w.y0) * w.w + (x - w.x0)] : 0.0f;
 }
 
 // ---------------------------------------------------------------------------
-__global__ void k_warp(ComposeArgs a) {
-    const int c = blockIdx.z;
-    const Win w = a.win[c * a.levels];
-    const int lx = blockIdx.x * blockDim.x + threadIdx.x, ly = blockIdx.y * blockDim.y + threadIdx.y;
-    if (lx >= w.w || ly >= w.h) return;
-    const int x = w.x0 + lx, y = w.y0 + ly;
-    const double* hi = a.hinv + c * 9;
-    const DevImage im = a.src[c];
-    const double X = static_cast<double>(x + a.origin_x), Y = static_cast<double>(y + a.origin_y);
-    const double wd = hi[6] * X + hi[7] * Y + hi[8];
-    const double sx = (hi[0] * X + hi[1] * Y + hi[2]) / wd;
-    const double sy = (hi[3] * X + hi[4] * Y + hi[5]) / wd;
-    float v = 0.0f;
-    uint8_t cv = 0;
-    if (!(sx < 0.0 || sx > im.w - 1 || sy < 0.0 || sy > im.h - 1)) {
-        const int x0 = static_cast<int>(sx), y0 = static_cast<int>(sy);
-        const double ax = sx - x0, ay = sy - y0;
-        const int x1 = min(x0 + 1, im.w - 1), y1 = min(y0 + 1, im.h - 1);
-        const uint8_t* r0 = im.p + static_cast<size_t>(y0) * im.w;
-        const uint8_t* r1 = im.p + static_cast<size_t>(y1) * im.w;
-        const double v00 = __ldg(r0 + x0), v10 = __ldg(r0 + x1);
-        const double v01 = __ldg(r1 + x0), v11 = __ldg(r1 + x1);
-        v = __double2float_rn((1 - ay) * ((1 - ax) * v00 + ax * v10) + ay * ((1 - ax) * v01 + ax * v11));
-        cv = 1;
-    }
-    a.G[c * a.levels][static_cast<size_t>(ly) * w.w + lx] = v;
-    a.cov[c][static_cast<size_t>(ly) * w.w + lx] = cv;
-}
-
-// one warp per (camera, window row): forward / backward run lengths by ballot
-template <typename CovT>
-__device__ void seam_row(const CovT* cov, float* dist, int w) {
-    const int lane = threadIdx.x & 31;
-    int carry = -1;  // last uncovered x (window-local); the outside counts as uncovered
-    for (int base = 0; base < w; base += 32) {
-        const int x = base + lane;
-        const bool covered = x < w && cov[x] > CovT(0);
-        const unsigned z = __ballot_sync(0xffffffffu, !covered);
-        const unsigned upto = z & (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u));
-        const int lz = upto ? base + 31 - __clz(upto) : carry;
-        if (x < w) dist[x] = static_cast<float>(x - lz);
-        if (z) carry = base + 31 - __clz(z);
-    }
-    int carry_r = w;  // next uncovered x
-    for (int base = ((w - 1) / 32) * 32; base >= 0; base -= 32) {
-        const int x = base + lane;
-        const bool covered = x < w && cov[x] > CovT(0);
-        const unsigned z = __ballot_sync(0xffffffffu, !covered);
-        const unsigned from = z & ~((1u << lane) - 1u);
-        const int nz = from ? base + __ffs(from) - 1 : carry_r;
-        if (x < w) {
-            const float b = static_cast<float>(nz - x);
-            const float f = dist[x];
-            dist[x] = b < f ? b : f;  // std::min(fwd, bwd)
-        }
-        if (z) carry_r = base + __ffs(z) - 1;
-    }
-}
-
-__global__ void k_seam_rows(ComposeArgs a) {
-    const int c = blockIdx.y;
-    const Win w = a.win[c * a.levels];
-    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (row >= w.h) return;
-    seam_row<uint8_t>(a.cov[c] + static_cast<size_t>(row) * w.w, a.M[c * a.levels] + static_cast<size_t>(row) * w.w,
-                      w.w);
-}
-
-__global__ void k_seam_norm(ComposeArgs a) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
-    if (x >= a.W[0] || y >= a.H[0]) return;
-    float sum = 0.0f;
-    for (int c = 0; c < a.ncams; ++c) {
-        const Win w = a.win[c * a.levels];
-        if (in_win(w, x, y)) sum = fadd(sum, a.M[c * a.levels][static_cast<size_t>(y - w.y0) * w.w + (x - w.x0)]);
-    }
-    if (!(sum > 0.0f)) return;
-    for (int c = 0; c < a.ncams; ++c) {
-        const Win w = a.win[c * a.levels];
-        if (in_win(w, x, y)) {
-            float* p = a.M[c * a.levels] + static_cast<size_t>(y - w.y0) * w.w + (x - w.x0);
-            *p = __fdiv_rn(*p, sum);
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// level k -> k+1 for both image and mask pyramids of one camera
-constexpr int PD_TX = 32, PD_TY = 8;
-constexpr int PD_IN_W = 2 * PD_TX + 6, PD_IN_H = 2 * PD_TY + 6;
-
-__global__ void __launch_bounds__(PD_TX * PD_TY) k_pyr_down(ComposeArgs a, int k) {
-    __shared__ float sG[PD_IN_H][PD_IN_W + 1];
-    __shared__ float sM[PD_IN_H][PD_IN_W + 1];
-    __shared__ float tG[PD_IN_H][PD_TX + 1];
-    __shared__ float tM[PD_IN_H][PD_TX + 1];
-    const int c = blockIdx.z;
-    const Win wi = a.win[c * a.levels + k], wo = a.win[c * a.levels + k + 1];
-    const int X0 = wo.x0 + blockIdx.x * PD_TX, Y0 = wo.y0 + blockIdx.y * PD_TY;
-    if (X0 >= wo.x0 + wo.w || Y0 >= wo.y0 + wo.h) return;
-    const float* Gi = a.G[c * a.levels + k];
-    const float* Mi = a.M[c * a.levels + k];
-    const int Wk = a.W[k], Hk = a.H[k];
-    const int xb = 2 * X0 - 3, yb = 2 * Y0 - 3;
-    const int tid = threadIdx.y * PD_TX + threadIdx.x;
-    for (int i = tid; i < PD_IN_H * PD_IN_W; i += PD_TX * PD_TY) {
-        const int r = i / PD_IN_W, cc = i - r * PD_IN_W;
-        const int gx = min(max(xb + cc, 0), Wk - 1), gy = min(max(yb + r, 0), Hk - 1);
-        sG[r][cc] = win_at(Gi, wi, gx, gy);
-        sM[r][cc] = win_at(Mi, wi, gx, gy);
-    }
-    __syncthreads();
-    float kt[7];
-#pragma unroll
-    for (int q = 0; q < 7; ++q) kt[q] = a.down_taps[q];
-    // horizontal blur at the even columns 2X (tmp rows cover 2Y-3 .. 2Y+3)
-    for (int i = tid; i < PD_IN_H * PD_TX; i += PD_TX * PD_TY) {
-        const int r = i / PD_TX, xo = i - r * PD_TX;
-        float g = 0.0f, m = 0.0f;
-#pragma unroll
-        for (int q = 0; q < 7; ++q) {
-            g = fadd(g, fmul(kt[q], sG[r][2 * xo + q]));
-            m = fadd(m, fmul(kt[q], sM[r][2 * xo + q]));
-        }
-        tG[r][xo] = g;
-        tM[r][xo] = m;
-    }
-    __syncthreads();
-    const int xo = threadIdx.x, yo = threadIdx.y;
-    const int X = X0 + xo, Y = Y0 + yo;
-    if (X >= wo.x0 + wo.w || Y >= wo.y0 + wo.h) return;
-    float g = 0.0f, m = 0.0f;
-#pragma unroll
-    for (int q = 0; q < 7; ++q) {
-        g = fadd(g, fmul(kt[q], tG[2 * yo + q][xo]));
-        m = fadd(m, fmul(kt[q], tM[2 * yo + q][xo]));
-    }
-    const size_t o = static_cast<size_t>(Y - wo.y0) * wo.w + (X - wo.x0);
-    a.G[c * a.levels + k + 1][o] = g;
-    a.M[c * a.levels + k + 1][o] = m;
-}
-
-// upsample (imgops.hpp:119-140) of a level-(k+1) raster read through `fetch`
+// upsample (imgops.hpp:119-140): align-corners float scale
 struct UpGeom {
     float sx, sy;
     int w, h;  // source (coarse) dims
@@ -192,6 +54,10 @@ __device__ __forceinline__ UpGeom up_geom(int w, int h, int tw, int th) {
     g.h = h;
     return g;
 }
+__device__ __forceinline__ float bilerp(float ax, float ay, float v00, float v10, float v01, float v11) {
+    const float oax = fsub(1.0f, ax), oay = fsub(1.0f, ay);
+    return fadd(fmul(oay, fadd(fmul(oax, v00), fmul(ax, v10))), fmul(ay, fadd(fmul(oax, v01), fmul(ax, v11))));
+}
 template <typename F>
 __device__ __forceinline__ float up_sample(const UpGeom& g, int x, int y, F fetch) {
     const float fx = fmul(static_cast<float>(x), g.sx), fy = fmul(static_cast<float>(y), g.sy);
@@ -199,10 +65,7 @@ __device__ __forceinline__ float up_sample(const UpGeom& g, int x, int y, F fetc
     const float ax = fsub(fx, static_cast<float>(x0)), ay = fsub(fy, static_cast<float>(y0));
     const int xa = min(max(x0, 0), g.w - 1), xb = min(max(x0 + 1, 0), g.w - 1);
     const int ya = min(max(y0, 0), g.h - 1), yb = min(max(y0 + 1, 0), g.h - 1);
-    const float v00 = fetch(xa, ya), v10 = fetch(xb, ya), v01 = fetch(xa, yb), v11 = fetch(xb, yb);
-    const float oax = fsub(1.0f, ax), oay = fsub(1.0f, ay);
-    return fadd(fmul(oay, fadd(fmul(oax, v00), fmul(ax, v10))),
-                fmul(ay, fadd(fmul(oax, v01), fmul(ax, v11))));
+    return bilerp(ax, ay, fetch(xa, ya), fetch(xb, ya), fetch(xa, yb), fetch(xb, yb));
 }
 
 __device__ __forceinline__ uint8_t to_u8(float v) {  // image.hpp:66-71
@@ -212,68 +75,347 @@ __device__ __forceinline__ uint8_t to_u8(float v) {  // image.hpp:66-71
     return static_cast<uint8_t>(r);
 }
 
-__global__ void k_blend_level(ComposeArgs a, int k) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
-    if (x >= a.W[k] || y >= a.H[k]) return;
-    const bool top = k == a.levels - 1;
-    const UpGeom ug = top ? UpGeom{0, 0, 1, 1} : up_geom(a.W[k + 1], a.H[k + 1], a.W[k], a.H[k]);
-    float acc = 0.0f, ws = 0.0f;
-    for (int c = 0; c < a.ncams; ++c) {
-        const Win w = a.win[c * a.levels + k];
-        if (!in_win(w, x, y)) continue;
-        const size_t o = static_cast<size_t>(y - w.y0) * w.w + (x - w.x0);
-        const float wt = a.M[c * a.levels + k][o];
-        float band = a.G[c * a.levels + k][o];
-        if (!top) {
-            const Win wn = a.win[c * a.levels + k + 1];
-            const float* Gn = a.G[c * a.levels + k + 1];
-            band = fsub(band, up_sample(ug, x, y, [&](int xx, int yy) { return win_at(Gn, wn, xx, yy); }));
-        }
-        ws = fadd(ws, wt);
-        acc = fadd(acc, fmul(wt, band));
+// distance of window-local (lx, ly) to its coverage run ends: the forward and
+// backward run lengths of linear_seam_mask (compose.hpp:108-120); 0 if uncovered
+__device__ __forceinline__ float run_dist(const ComposeArgs& a, int c, int ly, int lx) {
+    const int2 rr = a.run_rows[c][ly];
+    for (int i = 0; i < rr.y; ++i) {
+        const int2 r = a.runs[rr.x + i];
+        if (lx < r.x) break;
+        if (lx < r.y) return static_cast<float>(min(lx - r.x + 1, r.y - lx));
     }
-    if (ws > 1e-6f && fabsf(fsub(ws, 1.0f)) > 1e-6f) acc = __fdiv_rn(acc, ws);
-    if (!top) {
-        const float* Rn = a.R[k + 1];
-        const int wn = a.W[k + 1];
-        acc = fadd(acc, up_sample(ug, x, y, [&](int xx, int yy) { return Rn[static_cast<size_t>(yy) * wn + xx]; }));
-    }
-    if (k > 0)
-        a.R[k][static_cast<size_t>(y) * a.W[k] + x] = acc;
-    else
-        a.out[static_cast<size_t>(y) * a.W[0] + x] = ws > 0.0f ? to_u8(acc) : 0;
+    return 0.0f;
 }
 
-void blend_launch(const ComposeArgs& a, const Win* hw, cudaStream_t s) {
+// level-0 seam weight of camera `c` at canvas (x, y): dist_c / sum over cameras
+// in camera order (compose.hpp:123-129); cams: the candidate list (ordered)
+__device__ __forceinline__ float mask0_at(const ComposeArgs& a, int c, int x, int y, const int* cams, int nc) {
+    float sum = 0.0f, mine = 0.0f;
+    for (int i = 0; i < nc; ++i) {
+        const int k = cams[i];
+        const Win& w = a.win[k][0];
+        if (!in_win(w, x, y)) continue;
+        const float d = run_dist(a, k, y - w.y0, x - w.x0);
+        sum = fadd(sum, d);
+        if (k == c) mine = d;
+    }
+    return sum > 0.0f ? __fdiv_rn(mine, sum) : mine;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_warp(const __grid_constant__ ComposeArgs a) {
+    const int c = blockIdx.z;
+    const Win w = a.win[c][0];
+    const int lx = blockIdx.x * 32 + threadIdx.x, ly = blockIdx.y * blockDim.y + threadIdx.y;
+    const bool inb = lx < w.w && ly < w.h;
+    bool covered = false;
+    float v = 0.0f;
+    if (inb) {
+        const double* hi = a.hinv[c];
+        const DevImage im = a.src[c];
+        const double X = static_cast<double>(w.x0 + lx + a.origin_x), Y = static_cast<double>(w.y0 + ly + a.origin_y);
+        const double wd = hi[6] * X + hi[7] * Y + hi[8];
+        const double sx = (hi[0] * X + hi[1] * Y + hi[2]) / wd;
+        const double sy = (hi[3] * X + hi[4] * Y + hi[5]) / wd;
+        if (!(sx < 0.0 || sx > im.w - 1 || sy < 0.0 || sy > im.h - 1)) {
+            const int x0 = static_cast<int>(sx), y0 = static_cast<int>(sy);
+            const double ax = sx - x0, ay = sy - y0;
+            const int x1 = min(x0 + 1, im.w - 1), y1 = min(y0 + 1, im.h - 1);
+            const uint8_t* r0 = im.p + static_cast<size_t>(y0) * im.w;
+            const uint8_t* r1 = im.p + static_cast<size_t>(y1) * im.w;
+            const double v00 = __ldg(r0 + x0), v10 = __ldg(r0 + x1);
+            const double v01 = __ldg(r1 + x0), v11 = __ldg(r1 + x1);
+            v = __double2float_rn((1 - ay) * ((1 - ax) * v00 + ax * v10) + ay * ((1 - ax) * v01 + ax * v11));
+            covered = true;
+        }
+        a.G[c][0][static_cast<size_t>(ly) * w.w + lx] = v;
+    }
+    const unsigned bits = __ballot_sync(0xffffffffu, covered);
+    if (threadIdx.x == 0 && ly < w.h && blockIdx.x * 32 < w.w)
+        a.cov[c][static_cast<size_t>(ly) * a.cov_words[c] + blockIdx.x] = bits;
+}
+
+// warp per (camera, window row): covered runs from the coverage bit words
+__global__ void __launch_bounds__(256) k_runs(const __grid_constant__ ComposeArgs a) {
+    const int c = blockIdx.y;
+    const Win w = a.win[c][0];
+    const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (row >= w.h) return;
+    const int nw = a.cov_words[c];
+    const uint32_t* words = a.cov[c] + static_cast<size_t>(row) * nw;
+    auto starts_of = [&](int i) -> uint32_t {
+        if (i >= nw) return 0u;
+        const uint32_t cur = words[i], prev = i > 0 ? words[i - 1] : 0u;
+        return cur & ~((cur << 1) | (prev >> 31));
+    };
+    auto ends_of = [&](int i) -> uint32_t {
+        if (i >= nw) return 0u;
+        const uint32_t cur = words[i], next = i + 1 < nw ? words[i + 1] : 0u;
+        return cur & ~((cur >> 1) | (next << 31));
+    };
+    int total = 0;
+    for (int i = lane; i < nw; i += 32) total += __popc(starts_of(i));
+    for (int off = 16; off > 0; off >>= 1) total += __shfl_xor_sync(0xffffffffu, total, off);
+    int base = 0;
+    if (lane == 0) {
+        base = atomicAdd(a.runs_used, total);
+        if (base + total > a.runs_cap) {
+            dev_fail(a.status, LP_CAPACITY_OVERFLOW);
+            total = 0;
+        }
+        a.run_rows[c][row] = make_int2(base, total);
+    }
+    base = __shfl_sync(0xffffffffu, base, 0);
+    total = __shfl_sync(0xffffffffu, total, 0);
+    if (total == 0) return;
+    int ns = 0, ne = 0;  // runs started / ended before this chunk
+    for (int i0 = 0; i0 < nw; i0 += 32) {
+        const int i = i0 + lane;
+        uint32_t s = starts_of(i), e = ends_of(i);
+        const int cs = __popc(s), ce = __popc(e);
+        int ps = cs, pe = ce;  // inclusive prefix over lanes
+        for (int off = 1; off < 32; off <<= 1) {
+            const int ts = __shfl_up_sync(0xffffffffu, ps, off), te = __shfl_up_sync(0xffffffffu, pe, off);
+            if (lane >= off) {
+                ps += ts;
+                pe += te;
+            }
+        }
+        int ks = ns + ps - cs, ke = ne + pe - ce;
+        while (s) {
+            const int b = __ffs(s) - 1;
+            s &= s - 1;
+            a.runs[base + ks++].x = i * 32 + b;
+        }
+        while (e) {
+            const int b = __ffs(e) - 1;
+            e &= e - 1;
+            a.runs[base + ke++].y = i * 32 + b + 1;
+        }
+        ns += __shfl_sync(0xffffffffu, ps, 31);
+        ne += __shfl_sync(0xffffffffu, pe, 31);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// level k -> k+1 for both image and mask pyramids of one camera
+constexpr int PD_TX = 32, PD_TY = 8;
+constexpr int PD_IN_W = 2 * PD_TX + 6, PD_IN_H = 2 * PD_TY + 6;
+
+__global__ void __launch_bounds__(PD_TX * PD_TY) k_pyr_down(const __grid_constant__ ComposeArgs a, int k) {
+    __shared__ float sG[PD_IN_H][PD_IN_W + 1];
+    __shared__ float sM[PD_IN_H][PD_IN_W + 1];
+    __shared__ float tG[PD_IN_H][PD_TX + 1];
+    __shared__ float tM[PD_IN_H][PD_TX + 1];
+    __shared__ int s_cams[kMaxCompCams];
+    __shared__ int s_nc;
+    const int c = blockIdx.z;
+    const Win wi = a.win[c][k], wo = a.win[c][k + 1];
+    const int X0 = wo.x0 + blockIdx.x * PD_TX, Y0 = wo.y0 + blockIdx.y * PD_TY;
+    if (X0 >= wo.x0 + wo.w || Y0 >= wo.y0 + wo.h) return;
+    const float* Gi = a.G[c][k];
+    const float* Mi = a.M[c][k];
+    const int Wk = a.W[k], Hk = a.H[k];
+    const int xb = 2 * X0 - 3, yb = 2 * Y0 - 3;
+    const int tid = threadIdx.y * PD_TX + threadIdx.x;
+    const bool analytic = k == 0 && a.analytic_masks;
+    if (tid == 0) {
+        int n = 0;
+        if (analytic)
+            for (int q = 0; q < a.ncams; ++q) {
+                const Win& w = a.win[q][0];
+                if (w.w > 0 && w.h > 0 && w.x0 <= xb + PD_IN_W && w.x0 + w.w > xb - 1 && w.y0 <= yb + PD_IN_H &&
+                    w.y0 + w.h > yb - 1)
+                    s_cams[n++] = q;
+            }
+        s_nc = n;
+    }
+    __syncthreads();
+    for (int i = tid; i < PD_IN_H * PD_IN_W; i += PD_TX * PD_TY) {
+        const int r = i / PD_IN_W, cc = i - r * PD_IN_W;
+        const int gx = min(max(xb + cc, 0), Wk - 1), gy = min(max(yb + r, 0), Hk - 1);
+        sG[r][cc] = win_at(Gi, wi, gx, gy);
+        sM[r][cc] = analytic ? (in_win(wi, gx, gy) ? mask0_at(a, c, gx, gy, s_cams, s_nc) : 0.0f)
+                             : win_at(Mi, wi, gx, gy);
+    }
+    __syncthreads();
+    // horizontal blur at the even columns 2X (tmp rows cover 2Y-3 .. 2Y+3)
+    for (int i = tid; i < PD_IN_H * PD_TX; i += PD_TX * PD_TY) {
+        const int r = i / PD_TX, xo = i - r * PD_TX;
+        float g = 0.0f, m = 0.0f;
+#pragma unroll
+        for (int q = 0; q < 7; ++q) {
+            g = fadd(g, fmul(a.down_taps[q], sG[r][2 * xo + q]));
+            m = fadd(m, fmul(a.down_taps[q], sM[r][2 * xo + q]));
+        }
+        tG[r][xo] = g;
+        tM[r][xo] = m;
+    }
+    __syncthreads();
+    const int xo = threadIdx.x, yo = threadIdx.y;
+    const int X = X0 + xo, Y = Y0 + yo;
+    if (X >= wo.x0 + wo.w || Y >= wo.y0 + wo.h) return;
+    float g = 0.0f, m = 0.0f;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+        g = fadd(g, fmul(a.down_taps[q], tG[2 * yo + q][xo]));
+        m = fadd(m, fmul(a.down_taps[q], tM[2 * yo + q][xo]));
+    }
+    const size_t o = static_cast<size_t>(Y - wo.y0) * wo.w + (X - wo.x0);
+    a.G[c][k + 1][o] = g;
+    a.M[c][k + 1][o] = m;
+}
+
+// ---------------------------------------------------------------------------
+constexpr int BT_X = 64, BT_Y = 16;                      // level-k tile per CTA
+constexpr int BS_X = BT_X / 2 + 4, BS_Y = BT_Y / 2 + 4;  // staged level-(k+1) tile
+constexpr int BMAXC = 6;                                 // cameras staged per CTA
+
+__global__ void __launch_bounds__(256) k_blend_level(const __grid_constant__ ComposeArgs a, int k) {
+    __shared__ float sG[BMAXC][BS_Y][BS_X];
+    __shared__ float sR[BS_Y][BS_X];
+    __shared__ int s_cams[kMaxCompCams];
+    __shared__ int s_nc;
+    __shared__ int s_x0[BT_X], s_y0[BT_Y];
+    __shared__ float s_ax[BT_X], s_ay[BT_Y];
+    const int bx = blockIdx.x * BT_X, by = blockIdx.y * BT_Y;
+    const int Wk = a.W[k], Hk = a.H[k];
+    const bool top = k == a.levels - 1;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        int n = 0;
+        for (int q = 0; q < a.ncams; ++q) {
+            const Win& w = a.win[q][k];
+            if (w.w > 0 && w.h > 0 && w.x0 < bx + BT_X && w.x0 + w.w > bx && w.y0 < by + BT_Y && w.y0 + w.h > by)
+                s_cams[n++] = q;
+        }
+        s_nc = n;
+    }
+    UpGeom ug{0, 0, 1, 1};
+    if (!top) {
+        ug = up_geom(a.W[k + 1], a.H[k + 1], Wk, Hk);
+        if (tid < BT_X) {
+            const float fx = fmul(static_cast<float>(bx + tid), ug.sx);
+            const int x0 = static_cast<int>(fx);
+            s_x0[tid] = x0;
+            s_ax[tid] = fsub(fx, static_cast<float>(x0));
+        } else if (tid < BT_X + BT_Y) {
+            const int j = tid - BT_X;
+            const float fy = fmul(static_cast<float>(by + j), ug.sy);
+            const int y0 = static_cast<int>(fy);
+            s_y0[j] = y0;
+            s_ay[j] = fsub(fy, static_cast<float>(y0));
+        }
+    }
+    __syncthreads();
+    const int nc = s_nc;
+    const int nst = min(nc, BMAXC);
+    int lx0 = 0, ly0 = 0;
+    if (!top) {
+        lx0 = s_x0[0];
+        ly0 = s_y0[0];
+        const int W1 = a.W[k + 1], H1 = a.H[k + 1];
+        const float* Rn = a.R[k + 1];
+        for (int i = tid; i < (nst + 1) * BS_Y * BS_X; i += blockDim.x) {
+            const int slot = i / (BS_Y * BS_X), rem = i - slot * (BS_Y * BS_X);
+            const int r = rem / BS_X, q = rem - r * BS_X;
+            const int gx = min(max(lx0 + q, 0), W1 - 1), gy = min(max(ly0 + r, 0), H1 - 1);
+            if (slot < nst) {
+                const int cam = s_cams[slot];
+                sG[slot][r][q] = win_at(a.G[cam][k + 1], a.win[cam][k + 1], gx, gy);
+            } else {
+                sR[r][q] = Rn[static_cast<size_t>(gy) * W1 + gx];
+            }
+        }
+    }
+    __syncthreads();
+    const bool analytic = k == 0 && a.analytic_masks;
+    for (int p = tid; p < BT_X * BT_Y; p += blockDim.x) {
+        const int px = p % BT_X, py = p / BT_X;
+        const int x = bx + px, y = by + py;
+        if (x >= Wk || y >= Hk) continue;
+        int xa = 0, ya = 0;
+        float ax = 0.0f, ay = 0.0f;
+        if (!top) {
+            xa = s_x0[px] - lx0;
+            ya = s_y0[py] - ly0;
+            ax = s_ax[px];
+            ay = s_ay[py];
+        }
+        float sum = 0.0f;
+        if (analytic)
+            for (int i = 0; i < nc; ++i) {
+                const int cam = s_cams[i];
+                const Win& w = a.win[cam][0];
+                if (in_win(w, x, y)) sum = fadd(sum, run_dist(a, cam, y - w.y0, x - w.x0));
+            }
+        float acc = 0.0f, ws = 0.0f;
+        for (int i = 0; i < nc; ++i) {
+            const int cam = s_cams[i];
+            const Win& w = a.win[cam][k];
+            if (!in_win(w, x, y)) continue;
+            const size_t o = static_cast<size_t>(y - w.y0) * w.w + (x - w.x0);
+            float wt;
+            if (analytic) {
+                const float d = run_dist(a, cam, y - w.y0, x - w.x0);
+                wt = sum > 0.0f ? __fdiv_rn(d, sum) : d;
+            } else {
+                wt = a.M[cam][k][o];
+            }
+            float band = a.G[cam][k][o];
+            if (!top) {
+                float up;
+                if (i < BMAXC) {
+                    up = bilerp(ax, ay, sG[i][ya][xa], sG[i][ya][xa + 1], sG[i][ya + 1][xa], sG[i][ya + 1][xa + 1]);
+                } else {  // more cameras than staged slots: read through the cache
+                    const Win& wn = a.win[cam][k + 1];
+                    const float* Gn = a.G[cam][k + 1];
+                    up = up_sample(ug, x, y, [&](int xx, int yy) { return win_at(Gn, wn, xx, yy); });
+                }
+                band = fsub(band, up);
+            }
+            ws = fadd(ws, wt);
+            acc = fadd(acc, fmul(wt, band));
+        }
+        if (ws > 1e-6f && fabsf(fsub(ws, 1.0f)) > 1e-6f) acc = __fdiv_rn(acc, ws);
+        if (!top)
+            acc = fadd(acc, bilerp(ax, ay, sR[ya][xa], sR[ya][xa + 1], sR[ya + 1][xa], sR[ya + 1][xa + 1]));
+        if (k > 0)
+            a.R[k][static_cast<size_t>(y) * Wk + x] = acc;
+        else
+            a.out[static_cast<size_t>(y) * Wk + x] = ws > 0.0f ? to_u8(acc) : 0;
+    }
+}
+
+void blend_launch(const ComposeArgs& a, cudaStream_t s) {
     for (int k = 0; k + 1 < a.levels; ++k) {
         int mw = 0, mh = 0;
         for (int c = 0; c < a.ncams; ++c) {
-            mw = std::max(mw, hw[c * a.levels + k + 1].w);
-            mh = std::max(mh, hw[c * a.levels + k + 1].h);
+            mw = std::max(mw, a.win[c][k + 1].w);
+            mh = std::max(mh, a.win[c][k + 1].h);
         }
         if (mw == 0 || mh == 0) continue;
         dim3 grid(cdiv(mw, PD_TX), cdiv(mh, PD_TY), a.ncams);
         LPB_LAUNCH(k_pyr_down, grid, dim3(PD_TX, PD_TY), 0, s, a, k);
     }
     for (int k = a.levels - 1; k >= 0; --k) {
-        dim3 grid(cdiv(a.W[k], 32), cdiv(a.H[k], 8));
-        LPB_LAUNCH(k_blend_level, grid, dim3(32, 8), 0, s, a, k);
+        dim3 grid(cdiv(a.W[k], BT_X), cdiv(a.H[k], BT_Y));
+        LPB_LAUNCH(k_blend_level, grid, 256, 0, s, a, k);
     }
 }
 
-void compose_launch(const ComposeArgs& a, const Win* hw, cudaStream_t s) {
+void compose_launch(const ComposeArgs& a, cudaStream_t s) {
     int mw = 0, mh = 0;
     for (int c = 0; c < a.ncams; ++c) {
-        mw = std::max(mw, hw[c * a.levels].w);
-        mh = std::max(mh, hw[c * a.levels].h);
+        mw = std::max(mw, a.win[c][0].w);
+        mh = std::max(mh, a.win[c][0].h);
     }
+    LPB_CUDA(cudaMemsetAsync(a.runs_used, 0, sizeof(int), s));
     dim3 g0(cdiv(mw, 32), cdiv(mh, 8), a.ncams);
     LPB_LAUNCH(k_warp, g0, dim3(32, 8), 0, s, a);
     dim3 g1(cdiv(mh, 8), a.ncams);
-    LPB_LAUNCH(k_seam_rows, g1, 256, 0, s, a);
-    dim3 g2(cdiv(a.W[0], 32), cdiv(a.H[0], 8));
-    LPB_LAUNCH(k_seam_norm, g2, dim3(32, 8), 0, s, a);
-    blend_launch(a, hw, s);
+    LPB_LAUNCH(k_runs, g1, 256, 0, s, a);
+    blend_launch(a, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -311,12 +453,40 @@ void warp_generic_launch(const float* img, int w, int h, int ch, const double* h
     LPB_LAUNCH(k_warp_generic, g, dim3(32, 8), 0, s, img, w, h, ch, hinv, cw, chh, ox, oy, out, cov);
 }
 
+// linear_seam_mask (compose.hpp:101-131) on materialised float coverages:
+// one warp per (camera, row), ballot / clz run lengths
 __global__ void k_seam_generic_rows(const float* covs, int n, int w, int h, float* masks) {
     const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int c = blockIdx.y;
     if (row >= h) return;
     const size_t o = (static_cast<size_t>(c) * h + row) * w;
-    seam_row<float>(covs + o, masks + o, w);
+    const float* cov = covs + o;
+    float* dist = masks + o;
+    const int lane = threadIdx.x & 31;
+    int carry = -1;
+    for (int base = 0; base < w; base += 32) {
+        const int x = base + lane;
+        const bool covered = x < w && cov[x] > 0.0f;
+        const unsigned z = __ballot_sync(0xffffffffu, !covered);
+        const unsigned upto = z & (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u));
+        const int lz = upto ? base + 31 - __clz(upto) : carry;
+        if (x < w) dist[x] = static_cast<float>(x - lz);
+        if (z) carry = base + 31 - __clz(z);
+    }
+    int carry_r = w;
+    for (int base = ((w - 1) / 32) * 32; base >= 0; base -= 32) {
+        const int x = base + lane;
+        const bool covered = x < w && cov[x] > 0.0f;
+        const unsigned z = __ballot_sync(0xffffffffu, !covered);
+        const unsigned from = z & ~((1u << lane) - 1u);
+        const int nz = from ? base + __ffs(from) - 1 : carry_r;
+        if (x < w) {
+            const float b = static_cast<float>(nz - x);
+            const float f = dist[x];
+            dist[x] = b < f ? b : f;
+        }
+        if (z) carry_r = base + __ffs(z) - 1;
+    }
 }
 __global__ void k_seam_generic_norm(int n, int w, int h, float* masks) {
     const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -333,7 +503,6 @@ void seam_generic_launch(const float* covs, int n, int w, int h, float* masks, c
 }
 
 __global__ void k_down_h(const float* in, int w, int h, int ch, const float* taps, float* tmp) {
-    // horizontal σ=1 blur at even columns only: tmp is (w/2) x h x ch
     const int ow = w / 2;
     const long long n = static_cast<long long>(ow) * h * ch;
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;

@@ -10,26 +10,36 @@ struct Win {
     int x0, y0, w, h;
 };
 
+constexpr int kMaxCompCams = 16;   // cameras per rig on the fused compositor path
+constexpr int kMaxCompLevels = 12; // blend levels (canvas >= 2^11 px per side for 12)
+
+// Passed by value (constant bank): all per-camera geometry and pointers.
 struct ComposeArgs {
     int ncams, levels;
-    int W[kMaxLevels], H[kMaxLevels];     // canvas dims per level
+    int W[kMaxCompLevels], H[kMaxCompLevels];  // canvas dims per level
     int origin_x, origin_y;
-    const Win* win;                       // ncams * levels (device)
-    float* const* G;                      // ncams * levels image pyramid buffers (device ptrs)
-    float* const* M;                      // ncams * levels mask pyramid buffers
-    uint8_t* const* cov;                  // ncams coverage (level-0 window)
-    float* const* R;                      // levels collapse buffers (R[0] unused)
-    const float* down_taps;               // 7 taps of gaussian_kernel(1.0f)
-    // warp source: u8 grayscale cameras
-    const DevImage* src;                  // ncams (device)
-    const double* hinv;                   // ncams * 9 (device)
-    uint8_t* out;                         // W[0] x H[0]
+    int analytic_masks;   // 1: level-0 masks from coverage runs; 0: from M[c][0] buffers
+    Win win[kMaxCompCams][kMaxCompLevels];
+    float* G[kMaxCompCams][kMaxCompLevels];    // image pyramid windows
+    float* M[kMaxCompCams][kMaxCompLevels];    // mask pyramid windows (M[c][0] only if !analytic)
+    uint32_t* cov[kMaxCompCams];               // level-0 coverage bits, cov_words per window row
+    int cov_words[kMaxCompCams];
+    int2* run_rows[kMaxCompCams];              // per window row: (offset into runs, count)
+    int2* runs;                                // coverage runs [start, end) window-local
+    int runs_cap;
+    int* runs_used;
+    float* R[kMaxCompLevels];                  // collapse buffers, levels >= 1
+    float down_taps[7];                        // gaussian_kernel(1.0f)
+    DevImage src[kMaxCompCams];                // u8 grayscale cameras
+    double hinv[kMaxCompCams][9];
+    uint8_t* out;                              // W[0] x H[0]
+    int* status;
 };
 
-// Full per-frame compositor: warp, seam masks, pyramids, band blend + collapse.
-void compose_launch(const ComposeArgs& a, const Win* host_win, cudaStream_t s);
-// Pyramid + blend + collapse only (masks and level-0 images already in G/M).
-void blend_launch(const ComposeArgs& a, const Win* host_win, cudaStream_t s);
+// Full per-frame compositor: warp, coverage runs, pyramids, band blend + collapse.
+void compose_launch(const ComposeArgs& a, cudaStream_t s);
+// Pyramid + blend + collapse only (level-0 images and masks already in G/M).
+void blend_launch(const ComposeArgs& a, cudaStream_t s);
 
 // ---- stage-isolated primitives ----
 void warp_generic_launch(const float* img, int w, int h, int ch, const double* hinv, int cw, int chh,
