@@ -300,6 +300,9 @@ def main():
     roofline = None
     stage = {}
     if not args.no_profile:
+        # per-kernel times are taken with the stages serialised (one stream) so
+        # concurrent extraction does not inflate the compositor's kernels
+        lib.lp_rig_set_streams(rig.rig, 1)
         lib.lp_profile_reset()
         lib.lp_profile_enable(1)
         for i in range(args.steps):
@@ -312,6 +315,7 @@ def main():
         lib.lp_profile_read.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
         n = lib.lp_profile_read(names, 64, tot, cnt, cap)
         lib.lp_profile_enable(0)
+        lib.lp_rig_set_streams(rig.rig, 2)
         kern = {}
         for i in range(min(n, cap)):
             key = names.raw[i * 64:(i + 1) * 64].split(b"\0")[0].decode()

@@ -262,6 +262,9 @@ int lp_profile_read(char* names, int name_stride, double* total_ms, long long* l
 size_t lp_rig_panorama_capacity(lp_rig* rig);
 /* The stream the rig's work is enqueued on (cudaStream_t). */
 void* lp_rig_stream(lp_rig* rig);
+/* Frame scheduler: 2 (default) runs extraction on a second stream concurrently
+ * with warp/blend on cached-homography frames; 1 runs every stage in order. */
+lp_status lp_rig_set_streams(lp_rig* rig, int nstreams);
 
 #ifdef __cplusplus
 }

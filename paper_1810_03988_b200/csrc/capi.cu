@@ -595,6 +595,8 @@ lp_status lp_extract_features(lp_ctx* ctx, const uint8_t* img, int w, int h, int
         a.top_n = cfg->top_n;
         a.surv = surv.as<uint64_t>();
         a.surv_count = scount.as<unsigned>();
+        DBuf hist(sizeof(unsigned) * kTopnHistBins * nreg, s);
+        a.hist = hist.as<unsigned>();
         a.surv_cap = static_cast<int>(scap);
         a.kp_region = kpr.as<lp_keypoint>();
         a.count_region = cr.as<int>();
@@ -1024,13 +1026,15 @@ struct ComposeBuffers {
                 args.cov_words[c] = cdiv(w.w, 32);
                 args.cov[c] = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * args.cov_words[c] * std::max(w.h, 1)));
                 args.run_rows[c] = static_cast<int2*>(alloc(sizeof(int2) * std::max(w.h, 1)));
+                args.run_base[c] = static_cast<int>(total_rows * kRunSlots);
                 total_rows += w.h;
             }
         }
         for (int k = 1; k < levels; ++k)
             args.R[k] = static_cast<float*>(alloc(sizeof(float) * static_cast<size_t>(args.W[k]) * args.H[k]));
         if (analytic) {
-            args.runs_cap = static_cast<int>(std::min<size_t>(total_rows * 8 + 4096, 1u << 30));
+            args.runs_overflow_base = static_cast<int>(total_rows * kRunSlots);
+            args.runs_cap = static_cast<int>(std::min<size_t>(total_rows * (kRunSlots + 4) + 4096, 1u << 30));
             runs = DBuf(sizeof(int2) * args.runs_cap, s);
             runs_used = DBuf(sizeof(int), s);
             args.runs = runs.as<int2>();

@@ -87,19 +87,19 @@ __device__ __forceinline__ float run_dist(const ComposeArgs& a, int c, int ly, i
     return 0.0f;
 }
 
-// level-0 seam weight of camera `c` at canvas (x, y): dist_c / sum over cameras
-// in camera order (compose.hpp:123-129); cams: the candidate list (ordered)
-__device__ __forceinline__ float mask0_at(const ComposeArgs& a, int c, int x, int y, const int* cams, int nc) {
-    float sum = 0.0f, mine = 0.0f;
-    for (int i = 0; i < nc; ++i) {
-        const int k = cams[i];
-        const Win& w = a.win[k][0];
-        if (!in_win(w, x, y)) continue;
-        const float d = run_dist(a, k, y - w.y0, x - w.x0);
-        sum = fadd(sum, d);
-        if (k == c) mine = d;
-    }
-    return sum > 0.0f ? __fdiv_rn(mine, sum) : mine;
+// first coverage run of (camera, window row), staged in shared memory by the
+// consumers: (start, end, count); rows with more than one run use run_dist
+__device__ __forceinline__ int4 load_run_info(const ComposeArgs& a, int c, int ly) {
+    const Win& w = a.win[c][0];
+    if (ly < 0 || ly >= w.h) return make_int4(0, 0, 0, 0);
+    const int2 rr = a.run_rows[c][ly];
+    const int2 r = rr.y > 0 ? a.runs[rr.x] : make_int2(0, 0);
+    return make_int4(r.x, r.y, rr.y, 0);
+}
+__device__ __forceinline__ float dist_staged(const ComposeArgs& a, const int4& ri, int c, int ly, int lx) {
+    if (ri.z == 0) return 0.0f;
+    if (ri.z == 1) return (lx >= ri.x && lx < ri.y) ? static_cast<float>(min(lx - ri.x + 1, ri.y - lx)) : 0.0f;
+    return run_dist(a, c, ly, lx);
 }
 
 // ---------------------------------------------------------------------------
@@ -158,10 +158,14 @@ __global__ void __launch_bounds__(256) k_runs(const __grid_constant__ ComposeArg
     for (int off = 16; off > 0; off >>= 1) total += __shfl_xor_sync(0xffffffffu, total, off);
     int base = 0;
     if (lane == 0) {
-        base = atomicAdd(a.runs_used, total);
-        if (base + total > a.runs_cap) {
-            dev_fail(a.status, LP_CAPACITY_OVERFLOW);
-            total = 0;
+        if (total <= kRunSlots) {  // common case: no atomics
+            base = a.run_base[c] + kRunSlots * row;
+        } else {
+            base = a.runs_overflow_base + atomicAdd(a.runs_used, total);
+            if (base + total > a.runs_cap) {
+                dev_fail(a.status, LP_CAPACITY_OVERFLOW);
+                total = 0;
+            }
         }
         a.run_rows[c][row] = make_int2(base, total);
     }
@@ -209,6 +213,7 @@ __global__ void __launch_bounds__(PD_TX * PD_TY) k_pyr_down(const __grid_constan
     __shared__ float tM[PD_IN_H][PD_TX + 1];
     __shared__ int s_cams[kMaxCompCams];
     __shared__ int s_nc;
+    __shared__ int4 s_ri[kMaxCompCams][PD_IN_H];
     const int c = blockIdx.z;
     const Win wi = a.win[c][k], wo = a.win[c][k + 1];
     const int X0 = wo.x0 + blockIdx.x * PD_TX, Y0 = wo.y0 + blockIdx.y * PD_TY;
@@ -231,12 +236,36 @@ __global__ void __launch_bounds__(PD_TX * PD_TY) k_pyr_down(const __grid_constan
         s_nc = n;
     }
     __syncthreads();
+    const int nc = s_nc;
+    if (analytic)
+        for (int i = tid; i < nc * PD_IN_H; i += PD_TX * PD_TY) {
+            const int q = i / PD_IN_H, r = i - q * PD_IN_H;
+            const int cam = s_cams[q];
+            const int gy = min(max(yb + r, 0), Hk - 1);
+            s_ri[q][r] = load_run_info(a, cam, gy - a.win[cam][0].y0);
+        }
+    __syncthreads();
     for (int i = tid; i < PD_IN_H * PD_IN_W; i += PD_TX * PD_TY) {
         const int r = i / PD_IN_W, cc = i - r * PD_IN_W;
         const int gx = min(max(xb + cc, 0), Wk - 1), gy = min(max(yb + r, 0), Hk - 1);
         sG[r][cc] = win_at(Gi, wi, gx, gy);
-        sM[r][cc] = analytic ? (in_win(wi, gx, gy) ? mask0_at(a, c, gx, gy, s_cams, s_nc) : 0.0f)
-                             : win_at(Mi, wi, gx, gy);
+        float m = 0.0f;
+        if (!analytic) {
+            m = win_at(Mi, wi, gx, gy);
+        } else if (in_win(wi, gx, gy)) {
+            // linear_seam_mask weight (compose.hpp:123-129): dist_c / camera-ordered sum
+            float sum = 0.0f, mine = 0.0f;
+            for (int q = 0; q < nc; ++q) {
+                const int cam = s_cams[q];
+                const Win& w = a.win[cam][0];
+                if (!in_win(w, gx, gy)) continue;
+                const float d = dist_staged(a, s_ri[q][r], cam, gy - w.y0, gx - w.x0);
+                sum = fadd(sum, d);
+                if (cam == c) mine = d;
+            }
+            m = sum > 0.0f ? __fdiv_rn(mine, sum) : mine;
+        }
+        sM[r][cc] = m;
     }
     __syncthreads();
     // horizontal blur at the even columns 2X (tmp rows cover 2Y-3 .. 2Y+3)
@@ -278,6 +307,7 @@ __global__ void __launch_bounds__(256) k_blend_level(const __grid_constant__ Com
     __shared__ int s_nc;
     __shared__ int s_x0[BT_X], s_y0[BT_Y];
     __shared__ float s_ax[BT_X], s_ay[BT_Y];
+    __shared__ int4 s_ri[BMAXC][BT_Y];
     const int bx = blockIdx.x * BT_X, by = blockIdx.y * BT_Y;
     const int Wk = a.W[k], Hk = a.H[k];
     const bool top = k == a.levels - 1;
@@ -328,8 +358,14 @@ __global__ void __launch_bounds__(256) k_blend_level(const __grid_constant__ Com
             }
         }
     }
-    __syncthreads();
     const bool analytic = k == 0 && a.analytic_masks;
+    if (analytic)
+        for (int i = tid; i < nst * BT_Y; i += blockDim.x) {
+            const int q = i / BT_Y, r = i - q * BT_Y;
+            const int cam = s_cams[q];
+            s_ri[q][r] = load_run_info(a, cam, by + r - a.win[cam][0].y0);
+        }
+    __syncthreads();
     for (int p = tid; p < BT_X * BT_Y; p += blockDim.x) {
         const int px = p % BT_X, py = p / BT_X;
         const int x = bx + px, y = by + py;
@@ -343,11 +379,16 @@ __global__ void __launch_bounds__(256) k_blend_level(const __grid_constant__ Com
             ay = s_ay[py];
         }
         float sum = 0.0f;
+        float dl[BMAXC];
         if (analytic)
             for (int i = 0; i < nc; ++i) {
                 const int cam = s_cams[i];
                 const Win& w = a.win[cam][0];
-                if (in_win(w, x, y)) sum = fadd(sum, run_dist(a, cam, y - w.y0, x - w.x0));
+                if (!in_win(w, x, y)) continue;
+                const float d = i < BMAXC ? dist_staged(a, s_ri[i][py], cam, y - w.y0, x - w.x0)
+                                          : run_dist(a, cam, y - w.y0, x - w.x0);
+                if (i < BMAXC) dl[i] = d;
+                sum = fadd(sum, d);
             }
         float acc = 0.0f, ws = 0.0f;
         for (int i = 0; i < nc; ++i) {
@@ -357,7 +398,7 @@ __global__ void __launch_bounds__(256) k_blend_level(const __grid_constant__ Com
             const size_t o = static_cast<size_t>(y - w.y0) * w.w + (x - w.x0);
             float wt;
             if (analytic) {
-                const float d = run_dist(a, cam, y - w.y0, x - w.x0);
+                const float d = i < BMAXC ? dl[i] : run_dist(a, cam, y - w.y0, x - w.x0);
                 wt = sum > 0.0f ? __fdiv_rn(d, sum) : d;
             } else {
                 wt = a.M[cam][k][o];

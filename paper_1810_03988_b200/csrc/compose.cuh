@@ -12,6 +12,7 @@ struct Win {
 
 constexpr int kMaxCompCams = 16;   // cameras per rig on the fused compositor path
 constexpr int kMaxCompLevels = 12; // blend levels (canvas >= 2^11 px per side for 12)
+constexpr int kRunSlots = 4;       // coverage runs stored inline per window row
 
 // Passed by value (constant bank): all per-camera geometry and pointers.
 struct ComposeArgs {
@@ -25,9 +26,12 @@ struct ComposeArgs {
     uint32_t* cov[kMaxCompCams];               // level-0 coverage bits, cov_words per window row
     int cov_words[kMaxCompCams];
     int2* run_rows[kMaxCompCams];              // per window row: (offset into runs, count)
+    int run_base[kMaxCompCams];                // inline slots: row r of camera c owns
+                                               // runs[run_base[c] + kRunSlots*r ...]
     int2* runs;                                // coverage runs [start, end) window-local
-    int runs_cap;
-    int* runs_used;
+    int runs_cap;                              // inline slots + overflow area
+    int runs_overflow_base;
+    int* runs_used;                            // overflow allocations (rows with > kRunSlots runs)
     float* R[kMaxCompLevels];                  // collapse buffers, levels >= 1
     float down_taps[7];                        // gaussian_kernel(1.0f)
     DevImage src[kMaxCompCams];                // u8 grayscale cameras

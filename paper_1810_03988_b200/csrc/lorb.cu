@@ -182,6 +182,8 @@ __global__ void __launch_bounds__(256) k_detect(ExtractArgs a) {
                     a.surv[static_cast<size_t>(ri) * a.surv_cap + slot] = key;
                 else
                     dev_fail(a.status, LP_CAPACITY_OVERFLOW);
+                // first radix digit of k_topn: top 12 key bits (sign, exponent, 3 mantissa bits)
+                atomicAdd(&a.hist[static_cast<size_t>(ri) * kTopnHistBins + (key >> 52)], 1u);
             }
         }
     }
@@ -207,7 +209,129 @@ __device__ void bitonic_desc(uint64_t* v, int n_pow2) {
         }
 }
 
+// Fast path (top_n <= kTopnRankCap): the first radix digit (12 bits) comes
+// from the histogram k_detect built, refinement digits are 8 bits, and the
+// <= kTopnRankCap gathered keys are placed by rank (count of larger keys; keys
+// are unique), which needs no barriers and no sorting network.
 __global__ void __launch_bounds__(1024) k_topn(ExtractArgs a) {
+    __shared__ uint64_t s_keys[kTopnRankCap];
+    __shared__ unsigned s_hist[kTopnHistBins];
+    __shared__ unsigned s_wsum[32];
+    __shared__ uint64_t s_prefix;
+    __shared__ int s_pbits, s_k, s_bucket, s_m;
+    const int ri = blockIdx.x;
+    const int n = min(static_cast<int>(a.surv_count[ri]), a.surv_cap);
+    const uint64_t* keys = a.surv + static_cast<size_t>(ri) * a.surv_cap;
+    const int top_n = a.top_n;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int m;
+    if (n <= top_n) {
+        m = n;
+        for (int i = tid; i < n; i += blockDim.x) s_keys[i] = keys[i];
+    } else {
+        for (int i = tid; i < kTopnHistBins; i += blockDim.x)
+            s_hist[i] = a.hist[static_cast<size_t>(ri) * kTopnHistBins + i];
+        __syncthreads();
+        // descending-bin suffix scan: thread t owns bins 4095-4t .. 4092-4t
+        unsigned v[4], local = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            v[j] = s_hist[kTopnHistBins - 1 - (4 * tid + j)];
+            local += v[j];
+        }
+        unsigned incl = local;
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += t;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            unsigned ws = s_wsum[lane], wi = ws;
+            for (int off = 1; off < 32; off <<= 1) {
+                const unsigned t = __shfl_up_sync(0xffffffffu, wi, off);
+                if (lane >= off) wi += t;
+            }
+            s_wsum[lane] = wi - ws;  // exclusive
+        }
+        __syncthreads();
+        const unsigned excl = s_wsum[warp] + incl - local;
+        if (excl < static_cast<unsigned>(top_n) && static_cast<unsigned>(top_n) <= excl + local) {
+            unsigned cum = excl;
+            for (int j = 0; j < 4; ++j) {
+                if (cum + v[j] >= static_cast<unsigned>(top_n)) {
+                    s_prefix = static_cast<uint64_t>(kTopnHistBins - 1 - (4 * tid + j));
+                    s_k = top_n - static_cast<int>(cum);
+                    s_bucket = static_cast<int>(v[j]);
+                    s_pbits = 12;
+                    break;
+                }
+                cum += v[j];
+            }
+        }
+        __syncthreads();
+        // 8-bit refinement digits until the candidate set fits
+        while ((top_n - s_k) + s_bucket > kTopnRankCap && s_pbits < 64) {
+            const uint64_t prefix = s_prefix;
+            const int pbits = s_pbits;
+            const int dbits = pbits + 8 <= 64 ? 8 : 64 - pbits;
+            for (int i = tid; i < 256; i += blockDim.x) s_hist[i] = 0;
+            __syncthreads();
+            for (int i = tid; i < n; i += blockDim.x) {
+                const uint64_t k = keys[i];
+                if ((k >> (64 - pbits)) == prefix)
+                    atomicAdd(&s_hist[(k >> (64 - pbits - dbits)) & ((1u << dbits) - 1u)], 1u);
+            }
+            __syncthreads();
+            if (tid == 0) {
+                unsigned cum = 0;
+                int sel = 0;
+                for (int d = (1 << dbits) - 1; d >= 0; --d) {
+                    if (cum + s_hist[d] >= static_cast<unsigned>(s_k)) {
+                        sel = d;
+                        break;
+                    }
+                    cum += s_hist[d];
+                }
+                s_k -= static_cast<int>(cum);
+                s_bucket = static_cast<int>(s_hist[sel]);
+                s_prefix = (prefix << dbits) | static_cast<uint64_t>(sel);
+                s_pbits = pbits + dbits;
+            }
+            __syncthreads();
+        }
+        if (tid == 0) s_m = 0;
+        __syncthreads();
+        const uint64_t prefix = s_prefix;
+        const int sh = 64 - s_pbits;
+        for (int i = tid; i < n; i += blockDim.x) {
+            const uint64_t k = keys[i];
+            if ((sh == 64 ? 0 : (k >> sh)) >= prefix) {
+                const int slot = atomicAdd(&s_m, 1);
+                if (slot < kTopnRankCap) s_keys[slot] = k;
+            }
+        }
+        __syncthreads();
+        m = min(s_m, kTopnRankCap);
+    }
+    __syncthreads();
+    const int out_n = min(m, top_n);
+    for (int i = tid; i < m; i += blockDim.x) {
+        const uint64_t key = s_keys[i];
+        int r = 0;
+        for (int j = 0; j < m; ++j) r += s_keys[j] > key;
+        if (r < out_n) {
+            float resp;
+            int x, y;
+            kp_unkey(key, &resp, &x, &y);
+            a.kp_region[static_cast<size_t>(ri) * top_n + r] = lp_keypoint{x, y, resp, ri};
+        }
+    }
+    if (tid == 0) a.count_region[ri] = out_n;
+}
+
+// General path (any top_n <= kTopnSortCap): MSB radix select + bitonic sort.
+__global__ void __launch_bounds__(1024) k_topn_radix(ExtractArgs a) {
     extern __shared__ uint64_t s_keys[];  // kTopnSortCap
     __shared__ unsigned s_hist[256];
     __shared__ uint64_t s_prefix;
@@ -386,10 +510,15 @@ __global__ void __launch_bounds__(256) k_describe(ExtractArgs a, int warp_bytes)
 void extract_launch(const ExtractArgs& a, cudaStream_t s) {
     if (a.nregions == 0) return;
     LPB_CUDA(cudaMemsetAsync(a.surv_count, 0, sizeof(unsigned) * a.nregions, s));
+    LPB_CUDA(cudaMemsetAsync(a.hist, 0, sizeof(unsigned) * kTopnHistBins * a.nregions, s));
     if (a.total_tiles > 0) LPB_LAUNCH(k_detect, a.total_tiles, 256, 0, s, a);
-    const int topn_smem = kTopnSortCap * sizeof(uint64_t);
-    LPB_CUDA(cudaFuncSetAttribute(k_topn, cudaFuncAttributeMaxDynamicSharedMemorySize, topn_smem));
-    LPB_LAUNCH(k_topn, a.nregions, 1024, topn_smem, s, a);
+    if (a.top_n <= kTopnRankCap) {
+        LPB_LAUNCH(k_topn, a.nregions, 1024, 0, s, a);
+    } else {
+        const int topn_smem = kTopnSortCap * sizeof(uint64_t);
+        LPB_CUDA(cudaFuncSetAttribute(k_topn_radix, cudaFuncAttributeMaxDynamicSharedMemorySize, topn_smem));
+        LPB_LAUNCH(k_topn_radix, a.nregions, 1024, topn_smem, s, a);
+    }
     const int P = a.patch_half, RB = a.blur_r;
     const int pw = 2 * P + 1, iw = pw + 2 * RB;
     const int warp_bytes = (((iw * iw + 15) & ~15) + (iw * pw + pw * pw) * 4 + 15) & ~15;

@@ -18,6 +18,8 @@ constexpr int kDetTile = 32;     // output tile edge of the detect kernel
 constexpr int kMaxHarrisR = 6;   // harris_sigma <= 2 (radius ceil(3 sigma))
 constexpr int kMaxBlurR = 12;    // brief_blur_sigma <= 4
 constexpr int kTopnSortCap = 8192;
+constexpr int kTopnRankCap = 2048;   // k_topn fast path: rank placement of <= 2048 keys
+constexpr int kTopnHistBins = 4096;  // first radix digit: top 12 key bits
 
 // Everything the fused extractor needs, all device pointers.
 struct ExtractArgs {
@@ -32,6 +34,7 @@ struct ExtractArgs {
     int top_n;
     uint64_t* surv;          // nregions * surv_cap survivor keys
     unsigned* surv_count;    // nregions
+    unsigned* hist;          // nregions * kTopnHistBins (top-12-bit key histogram)
     int surv_cap;
     lp_keypoint* kp_region;  // nregions * top_n
     int* count_region;       // nregions

@@ -60,6 +60,14 @@ def load():
         lib.lp_rig_panorama_capacity.restype = C.c_size_t
         lib.lp_rig_stream.argtypes = [P]
         lib.lp_rig_stream.restype = P
+        lib.lp_rig_set_streams.argtypes = [P, C.c_int]
+        lib.lp_rig_set_streams.restype = C.c_int
+        lib.lp_rig_algorithmic_bytes.argtypes = [P, C.c_char_p]
+        lib.lp_rig_algorithmic_bytes.restype = C.c_double
+        lib.lp_profile_enable.argtypes = [C.c_int]
+        lib.lp_profile_enable.restype = None
+        lib.lp_profile_reset.argtypes = []
+        lib.lp_profile_reset.restype = None
         _lib = lib
         return lib
 

@@ -108,6 +108,20 @@ def test_extract_features_full_frame_region(lp, orc, params):
     assert np.array_equal(ka, kb) and np.array_equal(da, db)
 
 
+@pytest.mark.parametrize("top_n", [4, 37, 2048, 3000])
+def test_extract_top_n_paths(lp, orc, params, top_n):
+    """Histogram + rank top-N (top_n <= 2048) and the radix/bitonic path (> 2048)."""
+    from oracle.oracle import Oracle  # noqa: F401
+    img = orc.texture(700, 500, 13)
+    cfg = orc.default_params().extraction
+    cfg.top_n = top_n
+    pat = orc.brief_pattern(cfg.n_d, cfg.patch_half, 42)
+    reg = [(15, 15, 685, 485, 0), (100, 40, 300, 200, 0)]
+    ka, da = lp.extract_features(img, reg, cfg, pat)
+    kb, db = orc.extract_features(img, reg, cfg, pat)
+    assert np.array_equal(ka, kb) and np.array_equal(da, db)
+
+
 # ---------------------------------------------------------------- matching
 def _descs(orc, params, w=640, h=480):
     l, r, _ = orc.planted_pair(w, h, 0.25, 42)
