@@ -723,6 +723,14 @@ static double dot_blocked(const double* a, int sa, const double* b, int sb, int 
         for (int l = 0; l < s; ++l) p[l] += p[l + s];
     return p[0];
 }
+/* column dot product of the 9x9 Jacobi factor, fixed pairwise-tree order
+ * (shim: oracle/shim/Eigen/Dense dot9) */
+static double dot9(const double* r, int c0, int c1) {
+    double p[9];
+    for (int i = 0; i < 9; ++i) p[i] = r[i * 9 + c0] * r[i * 9 + c1];
+    return (((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]))) + p[8];
+}
+
 /* a: m x 9 row-major (modified). Writes V column of the smallest singular value. */
 static void svd_null_vector(double* a, int m, double* hv) {
     enum { N = 9 };
@@ -760,12 +768,7 @@ static void svd_null_vector(double* a, int m, double* hv) {
         int rotated = 0;
         for (int p = 0; p < N - 1; ++p)
             for (int q = p + 1; q < N; ++q) {
-                double al = 0, be = 0, ga = 0;
-                for (int i = 0; i < N; ++i) {
-                    al += r[i * N + p] * r[i * N + p];
-                    be += r[i * N + q] * r[i * N + q];
-                    ga += r[i * N + p] * r[i * N + q];
-                }
+                const double al = dot9(r, p, p), be = dot9(r, q, q), ga = dot9(r, p, q);
                 if (ga == 0.0 || fabs(ga) <= eps * sqrt(al * be)) continue;
                 rotated = 1;
                 const double zeta = (be - al) / (2.0 * ga);
@@ -786,11 +789,7 @@ static void svd_null_vector(double* a, int m, double* hv) {
         if (!rotated) break;
     }
     double sv[N];
-    for (int j = 0; j < N; ++j) {
-        double s = 0;
-        for (int i = 0; i < N; ++i) s += r[i * N + j] * r[i * N + j];
-        sv[j] = sqrt(s);
-    }
+    for (int j = 0; j < N; ++j) sv[j] = sqrt(dot9(r, j, j));
     /* stable descending order; take the last column */
     int order[N];
     for (int i = 0; i < N; ++i) order[i] = i;

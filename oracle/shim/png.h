@@ -44,4 +44,21 @@ inline void png_read_update_info(png_structp, png_infop) {}
 inline int png_get_channels(png_structp, png_infop) { return 1; }
 inline void png_read_image(png_structp, png_bytep*) {}
 
+/* writer side, used only by the reference's own PNG round-trip test
+ * (tests/test_imgcore.cpp:84-105): accepted and discarded, so that test
+ * fails cleanly (no libpng here) instead of crashing */
+#define PNG_INTERLACE_NONE 0
+#define PNG_COMPRESSION_TYPE_DEFAULT 0
+#define PNG_FILTER_TYPE_DEFAULT 0
+#define PNG_COLOR_TYPE_RGB 2
+inline png_structp png_create_write_struct(const char*, void*, void*, void*) {
+    static png_struct_def dummy;
+    return &dummy;
+}
+inline void png_set_IHDR(png_structp, png_infop, png_uint_32, png_uint_32, int, int, int, int, int) {}
+inline void png_write_info(png_structp, png_infop) {}
+inline void png_write_row(png_structp, const png_byte*) {}
+inline void png_write_end(png_structp, png_infop) {}
+inline void png_destroy_write_struct(png_structpp, png_infopp) {}
+
 #endif

@@ -726,7 +726,7 @@ lp_status lp_dlt_homography(lp_ctx* ctx, const lp_corr* pairs, int n, lp_homogra
         if (n < 4) throw Status(LP_INSUFFICIENT_MATCHES, "dlt: need at least 4 pairs");
         cudaStream_t s = ctx->stream;
         In<lp_corr> dc(pairs, n, s);
-        DBuf scratch(sizeof(double) * (static_cast<size_t>(2 * n) * 9 + 2 * n + n), s), dh(sizeof(lp_homography), s);
+        DBuf scratch(sizeof(double) * prosac_scratch_doubles(n), s), dh(sizeof(lp_homography), s);
         DevStatus st(s);
         dlt_launch(dc.d, n, scratch.as<double>(), dh.as<lp_homography>(), st.ptr(), s);
         sync_and_check(s, st.ptr());
@@ -749,7 +749,7 @@ lp_status lp_prosac_homography(lp_ctx* ctx, const lp_corr* matches, int n, const
         }
         In<lp_corr> dc(matches, n, s);
         const int mi = std::max(cfg->max_iter, 1);
-        DBuf drow = upload(row, s), cnt(sizeof(int), s), scratch(sizeof(double) * (static_cast<size_t>(2 * n) * 9 + 3 * n), s),
+        DBuf drow = upload(row, s), cnt(sizeof(int), s), scratch(sizeof(double) * prosac_scratch_doubles(n), s),
             dm(sizeof(lp_homography), s), dmask(n, s), dic(sizeof(int), s), dit(sizeof(int), s),
             tp(sizeof(int) * mi, s), ts(sizeof(int) * mi * 4, s);
         DevStatus pst(s);

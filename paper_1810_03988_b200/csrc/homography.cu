@@ -5,16 +5,19 @@
 //    128-bit product via __umul64hi) and the Chum-Matas growth schedule are
 //    replayed bit-exactly by one thread (homography.hpp:188-222);
 //  * hypotheses: chunks of 8 iterations, one warp each: the 4-point DLT
-//    (Hartley normalisation, 8x9 system, one-sided Jacobi SVD of the padded
-//    9x9, denormalisation, h33 scaling; homography.hpp:81-144) on lane 0, then
-//    warp-parallel symmetric-transfer-error scoring (147-152) with the inlier
-//    error sum accumulated in the reference's index order;
-//  * the sequential best-model / early-exit scan (248-261) on one thread, with
-//    the termination test read from a host-built glibc table (exact);
-//  * the final refit on all inliers: block-parallel Householder QR with the
-//    canonical 256-lane blocked dot product shared with the oracle's Eigen
-//    restatement, then the 9x9 Jacobi SVD (266-282).
+//    (Hartley normalisation, 8x9 system, one-sided Jacobi SVD; homography.hpp:
+//    81-144) with lane i owning row i of the 9x9 factor in registers and the
+//    column dot products reduced by shuffles in the fixed tree order the
+//    oracle's Eigen restatement uses; then warp-parallel symmetric transfer
+//    errors (147-152) with the inlier error sum accumulated in index order;
+//  * the sequential best-model / early-exit scan (248-261) on one thread, the
+//    termination test read from a host-built glibc table (exact);
+//  * the refit on all inliers (266-282): block-parallel inlier compaction,
+//    Householder QR with the canonical 256-lane blocked dot product, then the
+//    warp Jacobi SVD of the 9x9 factor.
 // Compiled with --fmad=false: every FP64 expression rounds like the x86 oracle.
+#include <cub/block/block_scan.cuh>
+
 #include "homography.cuh"
 
 namespace lpb {
@@ -97,60 +100,75 @@ struct Norm {
     double cx, cy, scale;
 };
 
-// one-sided Jacobi SVD of the 9x9 factor r (row-major), V column of the
-// smallest singular value -> hv. Mirrors oracle/shim/Eigen/Dense exactly.
-__device__ void jacobi_null_vector(double* r, double* hv) {
-    constexpr int N = 9;
-    double V[N * N];
-    for (int i = 0; i < N * N; ++i) V[i] = 0.0;
-    for (int i = 0; i < N; ++i) V[i * N + i] = 1.0;
+// ---- warp-parallel one-sided Jacobi SVD of a 9x9 factor ----
+constexpr unsigned kFull = 0xffffffffu;
+
+// sum of v over lanes 0..8 in the order (((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)))+p8
+// (oracle/shim/Eigen/Dense dot9); result broadcast to every lane
+__device__ __forceinline__ double tree9(double v) {
+    const double t = v + __shfl_down_sync(kFull, v, 1);
+    const double u = t + __shfl_down_sync(kFull, t, 2);
+    const double w = u + __shfl_down_sync(kFull, u, 4);
+    const double s = w + __shfl_sync(kFull, v, 8);
+    return __shfl_sync(kFull, s, 0);
+}
+
+// Lane i (< 9) holds row i of the factor in rr; lanes >= 9 hold zeros. On
+// return every lane holds the whole null vector hv (V column of the smallest
+// singular value, stable descending order as Eigen::JacobiSVD sorts).
+__device__ void warp_jacobi_null(double (&rr)[9], double (&hv)[9]) {
+    const int lane = threadIdx.x & 31;
+    double V[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) V[j] = lane == j ? 1.0 : 0.0;
     const double eps = 1e-15;
     for (int sweep = 0; sweep < 60; ++sweep) {
         bool rotated = false;
-        for (int p = 0; p < N - 1; ++p)
-            for (int q = p + 1; q < N; ++q) {
-                double al = 0, be = 0, ga = 0;
-                for (int i = 0; i < N; ++i) {
-                    al += r[i * N + p] * r[i * N + p];
-                    be += r[i * N + q] * r[i * N + q];
-                    ga += r[i * N + p] * r[i * N + q];
-                }
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+#pragma unroll
+            for (int q = p + 1; q < 9; ++q) {
+                const double al = tree9(rr[p] * rr[p]);
+                const double be = tree9(rr[q] * rr[q]);
+                const double ga = tree9(rr[p] * rr[q]);
                 if (ga == 0.0 || fabs(ga) <= eps * sqrt(al * be)) continue;
                 rotated = true;
                 const double zeta = (be - al) / (2.0 * ga);
                 const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                 const double c = 1.0 / sqrt(1.0 + t * t);
                 const double s = c * t;
-                for (int i = 0; i < N; ++i) {
-                    const double up = r[i * N + p], uq = r[i * N + q];
-                    r[i * N + p] = c * up - s * uq;
-                    r[i * N + q] = s * up + c * uq;
-                }
-                for (int i = 0; i < N; ++i) {
-                    const double vp = V[i * N + p], vq = V[i * N + q];
-                    V[i * N + p] = c * vp - s * vq;
-                    V[i * N + q] = s * vp + c * vq;
-                }
+                const double up = rr[p], uq = rr[q];
+                rr[p] = c * up - s * uq;
+                rr[q] = s * up + c * uq;
+                const double vp = V[p], vq = V[q];
+                V[p] = c * vp - s * vq;
+                V[q] = s * vp + c * vq;
             }
+        }
         if (!rotated) break;
     }
-    double sv[N];
-    for (int j = 0; j < N; ++j) {
-        double s = 0;
-        for (int i = 0; i < N; ++i) s += r[i * N + j] * r[i * N + j];
-        sv[j] = sqrt(s);
-    }
-    int order[N];
-    for (int i = 0; i < N; ++i) order[i] = i;
-    for (int i = 1; i < N; ++i) {
-        int x = order[i], j = i - 1;
+    double sv[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) sv[j] = sqrt(tree9(rr[j] * rr[j]));
+    int order[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) order[i] = i;
+    for (int i = 1; i < 9; ++i) {  // stable descending (insertion sort)
+        const int x = order[i];
+        int j = i - 1;
         while (j >= 0 && sv[x] > sv[order[j]]) {
             order[j + 1] = order[j];
             --j;
         }
         order[j + 1] = x;
     }
-    for (int i = 0; i < N; ++i) hv[i] = V[i * N + order[N - 1]];
+    const int jmin = order[8];
+    double mine = 0.0;
+#pragma unroll
+    for (int j = 0; j < 9; ++j)
+        if (j == jmin) mine = V[j];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) hv[i] = __shfl_sync(kFull, mine, i);
 }
 
 // denormalise H = Td^-1 * Hn * Ts, scale h33, degeneracy checks
@@ -193,13 +211,15 @@ __device__ int dlt_denormalize(const double* hv, Norm ns, Norm nd, double* H) {
     return LP_OK;
 }
 
-// 4-point DLT by one thread (homography.hpp:114-144 with n == 4)
-__device__ int dlt_minimal(const lp_corr* p, double* H) {
+// 4-point DLT by one warp (homography.hpp:114-144 with n == 4); every lane
+// returns the same status and H
+__device__ int dlt_minimal_warp(const lp_corr* p, double* H) {
+    const int lane = threadIdx.x & 31;
     for (int i = 0; i < 4; ++i)
         for (int j = i + 1; j < 4; ++j)
             for (int k = j + 1; k < 4; ++k) {
-                double cross = (p[j].sx - p[i].sx) * (p[k].sy - p[i].sy) -
-                               (p[j].sy - p[i].sy) * (p[k].sx - p[i].sx);
+                const double cross = (p[j].sx - p[i].sx) * (p[k].sy - p[i].sy) -
+                                     (p[j].sy - p[i].sy) * (p[k].sx - p[i].sx);
                 if (fabs(cross) < 1e-9) return LP_DEGENERATE_CONFIGURATION;
             }
     Norm ns{0, 0, 1}, nd{0, 0, 1};
@@ -225,24 +245,28 @@ __device__ int dlt_minimal(const lp_corr* p, double* H) {
     md /= 4.0;
     ns.scale = ms > 1e-12 ? sqrt(2.0) / ms : 1.0;
     nd.scale = md > 1e-12 ? sqrt(2.0) / md : 1.0;
-    double r[81];
-    for (int i = 0; i < 81; ++i) r[i] = 0.0;
-    for (int i = 0; i < 4; ++i) {
-        const double x = (p[i].sx - ns.cx) * ns.scale, y = (p[i].sy - ns.cy) * ns.scale;
-        const double u = (p[i].dx - nd.cx) * nd.scale, v = (p[i].dy - nd.cy) * nd.scale;
-        double* r0 = r + (2 * i) * 9;
-        double* r1 = r0 + 9;
-        r0[0] = -x; r0[1] = -y; r0[2] = -1; r0[6] = u * x; r0[7] = u * y; r0[8] = u;
-        r1[3] = -x; r1[4] = -y; r1[5] = -1; r1[6] = v * x; r1[7] = v * y; r1[8] = v;
+    double rr[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) rr[j] = 0.0;
+    if (lane < 8) {  // row `lane` of the 8x9 system (zero-padded to 9x9)
+        const lp_corr c = p[lane >> 1];
+        const double x = (c.sx - ns.cx) * ns.scale, y = (c.sy - ns.cy) * ns.scale;
+        const double u = (c.dx - nd.cx) * nd.scale, v = (c.dy - nd.cy) * nd.scale;
+        if ((lane & 1) == 0) {
+            rr[0] = -x; rr[1] = -y; rr[2] = -1; rr[6] = u * x; rr[7] = u * y; rr[8] = u;
+        } else {
+            rr[3] = -x; rr[4] = -y; rr[5] = -1; rr[6] = v * x; rr[7] = v * y; rr[8] = v;
+        }
     }
     double hv[9];
-    jacobi_null_vector(r, hv);
+    warp_jacobi_null(rr, hv);
     return dlt_denormalize(hv, ns, nd, H);
 }
 
 // ---- block-wide pieces (blockDim.x == 256) ----
 // canonical blocked dot products (oracle/shim/Eigen/Dense dot_blocked): lane
-// l = row & 255 accumulates rows in increasing order, then a pairwise tree.
+// l = row & 255 accumulates rows in increasing order, then the pairwise tree
+// p[l] += p[l+s], s = 128..1 (s >= 32 in shared memory, s <= 16 by shuffles)
 template <int K>
 __device__ void block_dots(const double* v, int sv, const double* const* cols, int sc, int r0,
                            int r1, double (*s_red)[256], double* out) {
@@ -260,12 +284,21 @@ __device__ void block_dots(const double* v, int sv, const double* const* cols, i
 #pragma unroll
     for (int k = 0; k < K; ++k) s_red[k][l] = p[k];
     __syncthreads();
-    for (int s = 128; s >= 1; s >>= 1) {
+    for (int s = 128; s >= 32; s >>= 1) {
         if (l < s)
 #pragma unroll
             for (int k = 0; k < K; ++k) s_red[k][l] = s_red[k][l] + s_red[k][l + s];
         __syncthreads();
     }
+    if (l < 32) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double x = s_red[k][l];
+            for (int s = 16; s >= 1; s >>= 1) x = x + __shfl_down_sync(kFull, x, s);
+            if (l == 0) s_red[k][0] = x;
+        }
+    }
+    __syncthreads();
 #pragma unroll
     for (int k = 0; k < K; ++k) out[k] = s_red[k][0];
     __syncthreads();
@@ -274,14 +307,14 @@ __device__ void block_dots(const double* v, int sv, const double* const* cols, i
 struct RefitShared {
     double red[8][256];
     double r[81];
-    double f[8];
-    double scal[4];
+    double H[9];
     Norm ns, nd;
     int status;
 };
 
-// dlt_homography over idx[0..m) of p (block-wide). A: 2m x 9 scratch, v: 2m scratch.
-__device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, double* vbuf,
+// dlt_homography over p[idx[0..m)] (block-wide). Scratch: A 2m x 9, vbuf 2m,
+// terms 2m. Returns the status on every thread; H valid on every thread.
+__device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, double* vbuf, double* terms,
                          double* H, RefitShared& sh) {
     const int tid = threadIdx.x;
     if (tid == 0) {
@@ -293,43 +326,51 @@ __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, dou
             for (int i = 0; i < 4 && sh.status == LP_OK; ++i)
                 for (int j = i + 1; j < 4; ++j)
                     for (int k = j + 1; k < 4; ++k) {
-                        double cross = (q[j].sx - q[i].sx) * (q[k].sy - q[i].sy) -
-                                       (q[j].sy - q[i].sy) * (q[k].sx - q[i].sx);
+                        const double cross = (q[j].sx - q[i].sx) * (q[k].sy - q[i].sy) -
+                                             (q[j].sy - q[i].sy) * (q[k].sx - q[i].sx);
                         if (fabs(cross) < 1e-9) sh.status = LP_DEGENERATE_CONFIGURATION;
                     }
         }
-        // hartley_normalizer, sequential sums (homography.hpp:81-97)
+        // hartley_normalizer centroids: sequential sums (homography.hpp:83-88)
         Norm ns{0, 0, 1}, nd{0, 0, 1};
         for (int i = 0; i < m; ++i) {
-            ns.cx += p[idx[i]].sx;
-            ns.cy += p[idx[i]].sy;
-        }
-        for (int i = 0; i < m; ++i) {
-            nd.cx += p[idx[i]].dx;
-            nd.cy += p[idx[i]].dy;
+            const lp_corr c = p[idx[i]];
+            ns.cx += c.sx;
+            ns.cy += c.sy;
+            nd.cx += c.dx;
+            nd.cy += c.dy;
         }
         ns.cx /= static_cast<double>(m);
         ns.cy /= static_cast<double>(m);
         nd.cx /= static_cast<double>(m);
         nd.cy /= static_cast<double>(m);
-        double ms = 0, md = 0;
-        for (int i = 0; i < m; ++i) {
-            double x = p[idx[i]].sx - ns.cx, y = p[idx[i]].sy - ns.cy;
-            ms += sqrt(x * x + y * y);
-        }
-        for (int i = 0; i < m; ++i) {
-            double x = p[idx[i]].dx - nd.cx, y = p[idx[i]].dy - nd.cy;
-            md += sqrt(x * x + y * y);
-        }
-        ms /= static_cast<double>(m);
-        md /= static_cast<double>(m);
-        ns.scale = ms > 1e-12 ? sqrt(2.0) / ms : 1.0;
-        nd.scale = md > 1e-12 ? sqrt(2.0) / md : 1.0;
         sh.ns = ns;
         sh.nd = nd;
     }
     __syncthreads();
     if (sh.status != LP_OK) return sh.status;
+    {
+        const Norm ns = sh.ns, nd = sh.nd;
+        for (int i = tid; i < m; i += blockDim.x) {  // distance terms, in parallel
+            const lp_corr c = p[idx[i]];
+            double x = c.sx - ns.cx, y = c.sy - ns.cy;
+            terms[i] = sqrt(x * x + y * y);
+            x = c.dx - nd.cx;
+            y = c.dy - nd.cy;
+            terms[m + i] = sqrt(x * x + y * y);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {  // mean distances: sequential sums (homography.hpp:89-95)
+        double ms = 0, md = 0;
+        for (int i = 0; i < m; ++i) ms += terms[i];
+        for (int i = 0; i < m; ++i) md += terms[m + i];
+        ms /= static_cast<double>(m);
+        md /= static_cast<double>(m);
+        sh.ns.scale = ms > 1e-12 ? sqrt(2.0) / ms : 1.0;
+        sh.nd.scale = md > 1e-12 ? sqrt(2.0) / md : 1.0;
+    }
+    __syncthreads();
     const Norm ns = sh.ns, nd = sh.nd;
     const int rows = 2 * m;
     for (int i = tid; i < m; i += blockDim.x) {
@@ -375,27 +416,54 @@ __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, dou
             __syncthreads();
         }
         for (int i = tid; i < 81; i += blockDim.x) {
-            int r = i / 9, c = i % 9;
+            const int r = i / 9, c = i % 9;
             sh.r[i] = c < r ? 0.0 : A[static_cast<size_t>(r) * 9 + c];
         }
     } else {
         for (int i = tid; i < 81; i += blockDim.x) {
-            int r = i / 9;
+            const int r = i / 9;
             sh.r[i] = r < rows ? A[i] : 0.0;
         }
     }
     __syncthreads();
-    if (tid == 0) {
-        double r[81], hv[9];
-        for (int i = 0; i < 81; ++i) r[i] = sh.r[i];
-        jacobi_null_vector(r, hv);
-        double Hh[9];
-        sh.status = dlt_denormalize(hv, ns, nd, Hh);
-        if (sh.status == LP_OK)
-            for (int i = 0; i < 9; ++i) H[i] = Hh[i];
+    if (tid < 32) {
+        double rr[9], hv[9];
+#pragma unroll
+        for (int j = 0; j < 9; ++j) rr[j] = tid < 9 ? sh.r[tid * 9 + j] : 0.0;
+        warp_jacobi_null(rr, hv);
+        if (tid == 0) {
+            double Hh[9];
+            sh.status = dlt_denormalize(hv, ns, nd, Hh);
+            for (int i = 0; i < 9; ++i) sh.H[i] = Hh[i];
+        }
     }
     __syncthreads();
-    return sh.status;
+    const int st = sh.status;
+    for (int i = 0; i < 9; ++i) H[i] = sh.H[i];
+    __syncthreads();
+    return st;
+}
+
+// order-preserving compaction of {i < n : flag(i)} into idx (block-wide);
+// returns the count on every thread
+template <typename F>
+__device__ int block_compact(int n, int* idx, F flag) {
+    using Scan = cub::BlockScan<int, 256>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int s_total;
+    int base = 0;
+    for (int b0 = 0; b0 < n; b0 += 256) {
+        const int i = b0 + threadIdx.x;
+        const int f = (i < n && flag(i)) ? 1 : 0;
+        int pos, total;
+        Scan(tmp).ExclusiveSum(f, pos, total);
+        if (f) idx[base + pos] = i;
+        if (threadIdx.x == 0) s_total = total;
+        __syncthreads();
+        base += s_total;
+        __syncthreads();
+    }
+    return base;
 }
 
 constexpr int kChunk = 8;  // hypotheses per round = warps per CTA
@@ -412,8 +480,9 @@ struct ProsacShared {
     double e[kChunk][32];
     uint8_t in[kChunk][32];
     double best_h[9], best_hi[9];
-    int best_count, iterations, done, n_in, final_count;
-    double H[9];
+    int best_count, iterations, done, final_count;
+    double H[9], Hi[9];
+    int refit_ok;
     RefitShared refit;
 };
 
@@ -475,36 +544,22 @@ __global__ void __launch_bounds__(256) k_prosac(ProsacArgs a) {
         }
         __syncthreads();
         if (warp < chunk) {
-            if (lane == 0) {
-                lp_corr q[4];
-                for (int i = 0; i < 4; ++i) q[i] = m[S.samples[warp][i]];
-                double H[9], Hi[9];
-                int ok = dlt_minimal(q, H) == LP_OK && h_inverse(H, Hi);
-                S.valid[warp] = ok;
-                if (ok)
-                    for (int i = 0; i < 9; ++i) {
-                        S.h[warp][i] = H[i];
-                        S.hi[warp][i] = Hi[i];
-                    }
-            }
-            __syncwarp();
-            if (S.valid[warp]) {
-                double hh[9], hhi[9];
-                for (int i = 0; i < 9; ++i) {
-                    hh[i] = S.h[warp][i];
-                    hhi[i] = S.hi[warp][i];
-                }
+            lp_corr q[4];
+            for (int i = 0; i < 4; ++i) q[i] = m[S.samples[warp][i]];
+            double H[9], Hi[9];
+            const bool ok = dlt_minimal_warp(q, H) == LP_OK && h_inverse(H, Hi);
+            if (ok) {
                 int count = 0;
                 double err = 0.0;
                 for (int base = 0; base < n; base += 32) {
                     const int i = base + lane;
                     if (i < n) {
-                        const double e = ste(hh, hhi, m[i]);
+                        const double e = ste(H, Hi, m[i]);
                         S.e[warp][lane] = e;
                         S.in[warp][lane] = e <= a.threshold;
                     }
                     __syncwarp();
-                    if (lane == 0) {
+                    if (lane == 0) {  // homography.hpp:240-247 order
                         const int lim = min(32, n - base);
                         for (int k = 0; k < lim; ++k)
                             if (S.in[warp][k]) {
@@ -517,8 +572,13 @@ __global__ void __launch_bounds__(256) k_prosac(ProsacArgs a) {
                 if (lane == 0) {
                     S.cnt[warp] = count;
                     S.err[warp] = err;
+                    for (int i = 0; i < 9; ++i) {
+                        S.h[warp][i] = H[i];
+                        S.hi[warp][i] = Hi[i];
+                    }
                 }
             }
+            if (lane == 0) S.valid[warp] = ok;
         }
         __syncthreads();
         if (tid == 0) {
@@ -557,41 +617,45 @@ __global__ void __launch_bounds__(256) k_prosac(ProsacArgs a) {
         return;
     }
     // refit on all inliers of the best hypothesis (homography.hpp:266-282)
-    double* A = a.scratch + static_cast<size_t>(pair) * (2 * a.cap * 9 + 2 * a.cap + a.cap);
+    double* A = a.scratch + static_cast<size_t>(pair) * prosac_scratch_doubles(a.cap);
     double* vbuf = A + static_cast<size_t>(2 * a.cap) * 9;
-    int* idx = reinterpret_cast<int*>(vbuf + 2 * a.cap);
+    double* terms = vbuf + 2 * a.cap;
+    int* idx = reinterpret_cast<int*>(terms + 2 * a.cap);
     uint8_t* mask = a.mask ? a.mask + static_cast<size_t>(pair) * a.cap : nullptr;
+    double bh[9], bhi[9];
+    for (int i = 0; i < 9; ++i) {
+        bh[i] = S.best_h[i];
+        bhi[i] = S.best_hi[i];
+    }
+    const int n_in = block_compact(n, idx, [&](int i) { return ste(bh, bhi, m[i]) <= a.threshold; });
+    double Hr[9], Hri[9];
+    const int st = dlt_block(m, idx, n_in, A, vbuf, terms, Hr, S.refit);
     if (tid == 0) {
-        int k = 0;
-        for (int i = 0; i < n; ++i)
-            if (ste(S.best_h, S.best_hi, m[i]) <= a.threshold) idx[k++] = i;
-        S.n_in = k;
+        S.refit_ok = st == LP_OK && h_inverse(Hr, Hri);
+        for (int i = 0; i < 9; ++i) {
+            S.H[i] = S.refit_ok ? Hr[i] : bh[i];
+            S.Hi[i] = S.refit_ok ? Hri[i] : bhi[i];
+        }
+        S.final_count = 0;
     }
     __syncthreads();
-    double Hr[9];
-    int st = dlt_block(m, idx, S.n_in, A, vbuf, Hr, S.refit);
+    double fh[9], fhi[9];
+    for (int i = 0; i < 9; ++i) {
+        fh[i] = S.H[i];
+        fhi[i] = S.Hi[i];
+    }
+    int local = 0;
+    for (int i = tid; i < n; i += blockDim.x) {
+        const bool in = ste(fh, fhi, m[i]) <= a.threshold;
+        if (mask) mask[i] = in;
+        local += in;
+    }
+    for (int off = 16; off > 0; off >>= 1) local += __shfl_xor_sync(kFull, local, off);
+    if (lane == 0) atomicAdd(&S.final_count, local);
+    __syncthreads();
     if (tid == 0) {
-        double Hri[9];
-        const double* use_h = S.best_h;
-        const double* use_hi = S.best_hi;
-        if (st == LP_OK && h_inverse(Hr, Hri)) {
-            for (int i = 0; i < 9; ++i) {
-                S.H[i] = Hr[i];
-                S.best_hi[i] = Hri[i];
-            }
-            use_h = S.H;
-        } else {
-            for (int i = 0; i < 9; ++i) S.H[i] = S.best_h[i];
-            use_h = S.H;
-        }
-        int cnt = 0;
-        for (int i = 0; i < n; ++i) {
-            bool in = ste(use_h, use_hi, m[i]) <= a.threshold;
-            if (mask) mask[i] = in;
-            cnt += in;
-        }
-        S.final_count = cnt;
-        for (int i = 0; i < 9; ++i) a.model[pair].h[i] = S.H[i];
+        const int cnt = S.final_count;
+        for (int i = 0; i < 9; ++i) a.model[pair].h[i] = fh[i];
         a.inlier_count[pair] = cnt;
         a.iterations[pair] = S.iterations;
         a.pair_status[pair] = cnt < 4 ? LP_NO_MODEL_FOUND : LP_OK;
@@ -644,11 +708,12 @@ __global__ void __launch_bounds__(256) k_dlt(const lp_corr* c, int n, double* sc
     __shared__ RefitShared sh;
     double* A = scratch;
     double* vbuf = A + static_cast<size_t>(2 * n) * 9;
-    int* idx = reinterpret_cast<int*>(vbuf + 2 * n);
+    double* terms = vbuf + 2 * n;
+    int* idx = reinterpret_cast<int*>(terms + 2 * n);
     for (int i = threadIdx.x; i < n; i += blockDim.x) idx[i] = i;
     __syncthreads();
     double H[9];
-    int st = dlt_block(c, idx, n, A, vbuf, H, sh);
+    const int st = dlt_block(c, idx, n, A, vbuf, terms, H, sh);
     if (threadIdx.x == 0) {
         *status = st;
         if (st == LP_OK)

@@ -28,6 +28,10 @@ struct ProsacArgs {
     int* pair_status;           // npairs: in = upstream status (0 ok), out = PROSAC status
 };
 
+// scratch doubles per pair: refit system A (2cap x 9), Householder vector
+// (2cap), Hartley distance terms (2cap), inlier index list (cap ints)
+__host__ __device__ inline size_t prosac_scratch_doubles(int cap) { return static_cast<size_t>(cap) * 24; }
+
 void prosac_launch(const ProsacArgs& a, cudaStream_t s);
 
 // chain[0] = I, chain[i+1] = chain[i] ∘ H_i (pipeline.hpp:474-493); any pair
