@@ -258,6 +258,16 @@ void lp_profile_reset(void);
  * summed ms, launch count; returns the number of distinct keys */
 int lp_profile_read(char* names, int name_stride, double* total_ms, long long* launches, int cap);
 
+/* Frames in flight (the pipelined mode of StitchEngine::run_pipelined,
+ * pipeline.hpp:660-711, as CUDA streams): enqueue ingest copy -> stages ->
+ * panorama egress for one frame and return immediately with a ticket; up to
+ * 3 frames overlap (copies in both directions run beside the stages).
+ * `panorama` (host or device, may be NULL) must stay valid until
+ * lp_rig_wait(ticket) returns; host buffers should be pinned for overlap. */
+lp_status lp_rig_submit(lp_rig* rig, const uint8_t* const* images, uint64_t frame_index,
+                        uint8_t* panorama, size_t pano_cap, uint64_t* ticket);
+lp_status lp_rig_wait(lp_rig* rig, uint64_t ticket, lp_canvas* canvas);
+
 /* Upper bound on panorama bytes for this rig's current homographies. */
 size_t lp_rig_panorama_capacity(lp_rig* rig);
 /* The stream the rig's work is enqueued on (cudaStream_t). */

@@ -763,13 +763,20 @@ static void svd_null_vector(double* a, int m, double* hv) {
     double V[N * N];
     memset(V, 0, sizeof V);
     for (int i = 0; i < N; ++i) V[i * N + i] = 1.0;
-    const double eps = 1e-15;
+    const double eps2 = 1e-30;
     for (int sweep = 0; sweep < 60; ++sweep) {
         int rotated = 0;
-        for (int p = 0; p < N - 1; ++p)
-            for (int q = p + 1; q < N; ++q) {
+        /* round-robin ordering (shim: oracle/shim/Eigen/Dense) */
+        for (int rnd = 0; rnd < 9; ++rnd)
+            for (int kk = 1; kk <= 4; ++kk) {
+                int p = (rnd + kk) % 9, q = (rnd - kk + 9) % 9;
+                if (p > q) {
+                    const int tmp = p;
+                    p = q;
+                    q = tmp;
+                }
                 const double al = dot9(r, p, p), be = dot9(r, q, q), ga = dot9(r, p, q);
-                if (ga == 0.0 || fabs(ga) <= eps * sqrt(al * be)) continue;
+                if (ga == 0.0 || ga * ga <= eps2 * (al * be)) continue;
                 rotated = 1;
                 const double zeta = (be - al) / (2.0 * ga);
                 const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));

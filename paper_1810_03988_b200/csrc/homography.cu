@@ -121,19 +121,30 @@ __device__ void warp_jacobi_null(double (&rr)[9], double (&hv)[9]) {
     double V[9];
 #pragma unroll
     for (int j = 0; j < 9; ++j) V[j] = lane == j ? 1.0 : 0.0;
-    const double eps = 1e-15;
+    const double eps2 = 1e-30;
     for (int sweep = 0; sweep < 60; ++sweep) {
         bool rotated = false;
+        // round-robin ordering shared with the oracles: round r rotates the
+        // four disjoint pairs {(r+k) mod 9, (r-k) mod 9}, k = 1..4, which
+        // commute exactly, so their 12 dot products and 4 rotations overlap
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
+        for (int rnd = 0; rnd < 9; ++rnd) {
+            double al[4], be[4], ga[4];
 #pragma unroll
-            for (int q = p + 1; q < 9; ++q) {
-                const double al = tree9(rr[p] * rr[p]);
-                const double be = tree9(rr[q] * rr[q]);
-                const double ga = tree9(rr[p] * rr[q]);
-                if (ga == 0.0 || fabs(ga) <= eps * sqrt(al * be)) continue;
+            for (int kk = 0; kk < 4; ++kk) {
+                const int a0 = (rnd + kk + 1) % 9, b0 = (rnd - kk - 1 + 9) % 9;
+                const int p = a0 < b0 ? a0 : b0, q = a0 < b0 ? b0 : a0;
+                al[kk] = tree9(rr[p] * rr[p]);
+                be[kk] = tree9(rr[q] * rr[q]);
+                ga[kk] = tree9(rr[p] * rr[q]);
+            }
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const int a0 = (rnd + kk + 1) % 9, b0 = (rnd - kk - 1 + 9) % 9;
+                const int p = a0 < b0 ? a0 : b0, q = a0 < b0 ? b0 : a0;
+                if (ga[kk] == 0.0 || ga[kk] * ga[kk] <= eps2 * (al[kk] * be[kk])) continue;
                 rotated = true;
-                const double zeta = (be - al) / (2.0 * ga);
+                const double zeta = (be[kk] - al[kk]) / (2.0 * ga[kk]);
                 const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                 const double c = 1.0 / sqrt(1.0 + t * t);
                 const double s = c * t;

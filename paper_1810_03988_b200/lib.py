@@ -60,6 +60,10 @@ def load():
         lib.lp_rig_panorama_capacity.restype = C.c_size_t
         lib.lp_rig_stream.argtypes = [P]
         lib.lp_rig_stream.restype = P
+        lib.lp_rig_submit.argtypes = [P, P, C.c_uint64, P, C.c_size_t, C.POINTER(C.c_uint64)]
+        lib.lp_rig_submit.restype = C.c_int
+        lib.lp_rig_wait.argtypes = [P, C.c_uint64, C.POINTER(abi.Canvas)]
+        lib.lp_rig_wait.restype = C.c_int
         lib.lp_rig_set_streams.argtypes = [P, C.c_int]
         lib.lp_rig_set_streams.restype = C.c_int
         lib.lp_rig_algorithmic_bytes.argtypes = [P, C.c_char_p]
@@ -157,6 +161,18 @@ class Rig:
 
     def panorama_capacity(self):
         return int(self.lib.lp_rig_panorama_capacity(self.rig))
+
+    def submit(self, image_ptrs, frame_index, pano_ptr=None, pano_cap=0):
+        """Asynchronous frame (lp_rig_submit): returns a ticket for wait()."""
+        arr = (C.c_void_p * self.ncams)(*image_ptrs)
+        t = C.c_uint64()
+        _check(self.lib, self.lib.lp_rig_submit(self.rig, arr, frame_index, pano_ptr, pano_cap, C.byref(t)))
+        return t.value
+
+    def wait(self, ticket):
+        cv = abi.Canvas()
+        _check(self.lib, self.lib.lp_rig_wait(self.rig, ticket, C.byref(cv)))
+        return (cv.width, cv.height, cv.origin_x, cv.origin_y)
 
     def stitch_raw(self, image_ptrs, frame_index, fo):
         """Zero-copy call: image_ptrs = list of addresses (host or device), fo a FrameOut."""

@@ -357,3 +357,27 @@ def test_errors_match_oracle(lp, orc):
                 f(o)
             names.append(e.value.name)
         assert names[0] == names[1], names
+
+
+def test_rig_frames_in_flight(lp, orc, params):
+    """lp_rig_submit / lp_rig_wait with 3 frames in flight: panoramas equal the
+    synchronous path frame by frame (host and device outputs)."""
+    import torch
+    from paper_1810_03988_b200 import Rig
+    p = orc.default_params()
+    p.seed = p.matching.seed = 42
+    p.homography_refresh = 1 << 30
+    frames = [orc.sequence_frame(480, 270, t, 0.25, 42) for t in range(5)]
+    want = []
+    ref_rig = Rig(lp, 2, 480, 270, p)
+    for t, (l, r) in enumerate(frames):
+        want.append(ref_rig.stitch([l, r], t)["panorama"])
+    rig = Rig(lp, 2, 480, 270, p)
+    cap = rig.panorama_capacity()
+    host = [torch.zeros(cap, dtype=torch.uint8).pin_memory() for _ in range(5)]
+    ins = [[torch.from_numpy(l).pin_memory(), torch.from_numpy(r).pin_memory()] for l, r in frames]
+    tickets = [rig.submit([a.data_ptr(), b.data_ptr()], t, host[t].data_ptr(), cap) for t, (a, b) in enumerate(ins)]
+    for t, tk in enumerate(tickets):
+        W, H, _, _ = rig.wait(tk)
+        got = host[t][:W * H].numpy().reshape(H, W)
+        assert np.array_equal(got, want[t]), t
