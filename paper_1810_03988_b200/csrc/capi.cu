@@ -11,6 +11,7 @@
 #include <cub/cub.cuh>
 
 #include <atomic>
+#include <deque>
 #include <map>
 #include <memory>
 #include <mutex>
