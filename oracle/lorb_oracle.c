@@ -776,7 +776,8 @@ static void svd_null_vector(double* a, int m, double* hv) {
                     q = tmp;
                 }
                 const double al = dot9(r, p, p), be = dot9(r, q, q), ga = dot9(r, p, q);
-                if (ga == 0.0 || ga * ga <= eps2 * (al * be)) continue;
+                if (ga == 0.0 || ga * ga <= eps2 * (al * be) || fabs(ga) <= 2.220446049250313e-16 * fmax(al, be))
+                    continue;
                 rotated = 1;
                 const double zeta = (be - al) / (2.0 * ga);
                 const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));

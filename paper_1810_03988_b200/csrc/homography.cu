@@ -142,7 +142,9 @@ __device__ void warp_jacobi_null(double (&rr)[9], double (&hv)[9]) {
             for (int kk = 0; kk < 4; ++kk) {
                 const int a0 = (rnd + kk + 1) % 9, b0 = (rnd - kk - 1 + 9) % 9;
                 const int p = a0 < b0 ? a0 : b0, q = a0 < b0 ? b0 : a0;
-                if (ga[kk] == 0.0 || ga[kk] * ga[kk] <= eps2 * (al[kk] * be[kk])) continue;
+                if (ga[kk] == 0.0 || ga[kk] * ga[kk] <= eps2 * (al[kk] * be[kk]) ||
+                    fabs(ga[kk]) <= 2.220446049250313e-16 * fmax(al[kk], be[kk]))
+                    continue;
                 rotated = true;
                 const double zeta = (be[kk] - al[kk]) / (2.0 * ga[kk]);
                 const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
