@@ -1018,7 +1018,7 @@ struct ComposeBuffers {
                 args.win[c][k] = w;
                 const size_t np = static_cast<size_t>(w.w) * w.h;
                 args.G[c][k] = static_cast<float*>(alloc(sizeof(float) * np));
-                if (k > 0 || !analytic) args.M[c][k] = static_cast<float*>(alloc(sizeof(float) * np));
+                args.M[c][k] = static_cast<float*>(alloc(sizeof(float) * np));
                 host_G[c * levels + k] = args.G[c][k];
                 host_M[c * levels + k] = args.M[c][k];
             }

@@ -13,13 +13,13 @@
 //   k_warp        FP64 inverse map + bilinear (compose.hpp:72-95) -> G0 window
 //                 and one coverage bit per pixel (warp ballot per 32 px)
 //   k_runs        warp per window row: covered runs [start,end) from the bit
-//                 words (start/end masks + warp prefix sums). The linear seam
-//                 mask (compose.hpp:101-131) is then analytic: distance to the
-//                 run ends, min(fwd, bwd), divided by the camera-ordered sum —
-//                 never materialised at level 0
+//                 words (start/end masks + warp prefix sums)
+//   k_mask0       the linear seam mask (compose.hpp:101-131) from the runs:
+//                 distance to the run ends, min(fwd, bwd), divided by the
+//                 camera-ordered sum, once per camera-window pixel
 //   k_pyr_down    (L-1)x: shared-memory tile; 7-tap σ=1 blur evaluated only at
 //                 the kept even samples (imgops.hpp:106-116); image and mask
-//                 pyramids in one pass (level-0 mask computed from the runs)
+//                 pyramids in one pass
 //   k_blend_level Lx, top to bottom: 64x16 tile per CTA; the CTA culls cameras
 //                 whose window misses the tile, stages the coarser level of
 //                 each remaining camera and the coarser collapse result in
@@ -202,6 +202,67 @@ __global__ void __launch_bounds__(256) k_runs(const __grid_constant__ ComposeArg
 }
 
 // ---------------------------------------------------------------------------
+// level-0 seam masks (compose.hpp:101-131), once per camera-window pixel:
+// distance to the pixel's coverage-run ends, divided by the camera-ordered
+// sum over every camera covering the pixel. Runs are staged per (camera,
+// row) in canvas coordinates, so no window tests are needed.
+constexpr int MK_TX = 64, MK_TY = 8;
+
+__global__ void __launch_bounds__(256) k_mask0(const __grid_constant__ ComposeArgs a) {
+    __shared__ int s_cams[kMaxCompCams];
+    __shared__ int s_nc;
+    __shared__ int4 s_run[kMaxCompCams][MK_TY];  // canvas [S, E), count
+    const int c = blockIdx.z;
+    const Win wc = a.win[c][0];
+    const int lx0 = blockIdx.x * MK_TX, ly0 = blockIdx.y * MK_TY;
+    if (lx0 >= wc.w || ly0 >= wc.h) return;
+    const int X0 = wc.x0 + lx0, Y0 = wc.y0 + ly0;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        int n = 0;
+        for (int q = 0; q < a.ncams; ++q) {
+            const Win& w = a.win[q][0];
+            if (w.w > 0 && w.h > 0 && w.x0 < X0 + MK_TX && w.x0 + w.w > X0 && w.y0 < Y0 + MK_TY && w.y0 + w.h > Y0)
+                s_cams[n++] = q;
+        }
+        s_nc = n;
+    }
+    __syncthreads();
+    const int nc = s_nc;
+    for (int i = tid; i < nc * MK_TY; i += blockDim.x) {
+        const int q = i / MK_TY, r = i - q * MK_TY;
+        const int cam = s_cams[q];
+        const Win& w = a.win[cam][0];
+        int4 ri = load_run_info(a, cam, Y0 + r - w.y0);
+        ri.x += w.x0;
+        ri.y += w.x0;
+        s_run[q][r] = ri;
+    }
+    __syncthreads();
+    for (int p = tid; p < MK_TX * MK_TY; p += blockDim.x) {
+        const int px = p % MK_TX, py = p / MK_TX;
+        const int lx = lx0 + px, ly = ly0 + py;
+        if (lx >= wc.w || ly >= wc.h) continue;
+        const int x = X0 + px, y = Y0 + py;
+        float sum = 0.0f, mine = 0.0f;
+        for (int q = 0; q < nc; ++q) {
+            const int4 ri = s_run[q][py];
+            float d;
+            if (ri.z <= 1) {
+                d = (ri.z == 1 && x >= ri.x && x < ri.y) ? static_cast<float>(min(x - ri.x + 1, ri.y - x)) : 0.0f;
+            } else {
+                const int cam = s_cams[q];
+                const Win& w = a.win[cam][0];
+                d = run_dist(a, cam, y - w.y0, x - w.x0);
+            }
+            sum = fadd(sum, d);
+            if (s_cams[q] == c) mine = d;
+        }
+        a.M[c][0][static_cast<size_t>(ly) * wc.w + lx] = sum > 0.0f ? __fdiv_rn(mine, sum) : mine;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // level k -> k+1 for both image and mask pyramids of one camera
 constexpr int PD_TX = 32, PD_TY = 8;
 constexpr int PD_IN_W = 2 * PD_TX + 6, PD_IN_H = 2 * PD_TY + 6;
@@ -211,9 +272,6 @@ __global__ void __launch_bounds__(PD_TX * PD_TY) k_pyr_down(const __grid_constan
     __shared__ float sM[PD_IN_H][PD_IN_W + 1];
     __shared__ float tG[PD_IN_H][PD_TX + 1];
     __shared__ float tM[PD_IN_H][PD_TX + 1];
-    __shared__ int s_cams[kMaxCompCams];
-    __shared__ int s_nc;
-    __shared__ int4 s_ri[kMaxCompCams][PD_IN_H];
     const int c = blockIdx.z;
     const Win wi = a.win[c][k], wo = a.win[c][k + 1];
     const int X0 = wo.x0 + blockIdx.x * PD_TX, Y0 = wo.y0 + blockIdx.y * PD_TY;
@@ -223,49 +281,24 @@ __global__ void __launch_bounds__(PD_TX * PD_TY) k_pyr_down(const __grid_constan
     const int Wk = a.W[k], Hk = a.H[k];
     const int xb = 2 * X0 - 3, yb = 2 * Y0 - 3;
     const int tid = threadIdx.y * PD_TX + threadIdx.x;
-    const bool analytic = k == 0 && a.analytic_masks;
-    if (tid == 0) {
-        int n = 0;
-        if (analytic)
-            for (int q = 0; q < a.ncams; ++q) {
-                const Win& w = a.win[q][0];
-                if (w.w > 0 && w.h > 0 && w.x0 <= xb + PD_IN_W && w.x0 + w.w > xb - 1 && w.y0 <= yb + PD_IN_H &&
-                    w.y0 + w.h > yb - 1)
-                    s_cams[n++] = q;
-            }
-        s_nc = n;
-    }
-    __syncthreads();
-    const int nc = s_nc;
-    if (analytic)
-        for (int i = tid; i < nc * PD_IN_H; i += PD_TX * PD_TY) {
-            const int q = i / PD_IN_H, r = i - q * PD_IN_H;
-            const int cam = s_cams[q];
-            const int gy = min(max(yb + r, 0), Hk - 1);
-            s_ri[q][r] = load_run_info(a, cam, gy - a.win[cam][0].y0);
+    // fast path: the whole staged rectangle lies inside the canvas and the window
+    const bool inside = xb >= wi.x0 && yb >= wi.y0 && xb + PD_IN_W <= wi.x0 + wi.w && yb + PD_IN_H <= wi.y0 + wi.h &&
+                        xb >= 0 && yb >= 0 && xb + PD_IN_W <= Wk && yb + PD_IN_H <= Hk;
+    if (inside) {
+        const float* g0 = Gi + (yb - wi.y0) * wi.w + (xb - wi.x0);
+        const float* m0 = Mi + (yb - wi.y0) * wi.w + (xb - wi.x0);
+        for (int i = tid; i < PD_IN_H * PD_IN_W; i += PD_TX * PD_TY) {
+            const int r = i / PD_IN_W, cc = i - r * PD_IN_W;
+            sG[r][cc] = g0[r * wi.w + cc];
+            sM[r][cc] = m0[r * wi.w + cc];
         }
-    __syncthreads();
-    for (int i = tid; i < PD_IN_H * PD_IN_W; i += PD_TX * PD_TY) {
-        const int r = i / PD_IN_W, cc = i - r * PD_IN_W;
-        const int gx = min(max(xb + cc, 0), Wk - 1), gy = min(max(yb + r, 0), Hk - 1);
-        sG[r][cc] = win_at(Gi, wi, gx, gy);
-        float m = 0.0f;
-        if (!analytic) {
-            m = win_at(Mi, wi, gx, gy);
-        } else if (in_win(wi, gx, gy)) {
-            // linear_seam_mask weight (compose.hpp:123-129): dist_c / camera-ordered sum
-            float sum = 0.0f, mine = 0.0f;
-            for (int q = 0; q < nc; ++q) {
-                const int cam = s_cams[q];
-                const Win& w = a.win[cam][0];
-                if (!in_win(w, gx, gy)) continue;
-                const float d = dist_staged(a, s_ri[q][r], cam, gy - w.y0, gx - w.x0);
-                sum = fadd(sum, d);
-                if (cam == c) mine = d;
-            }
-            m = sum > 0.0f ? __fdiv_rn(mine, sum) : mine;
+    } else {
+        for (int i = tid; i < PD_IN_H * PD_IN_W; i += PD_TX * PD_TY) {
+            const int r = i / PD_IN_W, cc = i - r * PD_IN_W;
+            const int gx = min(max(xb + cc, 0), Wk - 1), gy = min(max(yb + r, 0), Hk - 1);
+            sG[r][cc] = win_at(Gi, wi, gx, gy);
+            sM[r][cc] = win_at(Mi, wi, gx, gy);
         }
-        sM[r][cc] = m;
     }
     __syncthreads();
     // horizontal blur at the even columns 2X (tmp rows cover 2Y-3 .. 2Y+3)
@@ -290,7 +323,7 @@ __global__ void __launch_bounds__(PD_TX * PD_TY) k_pyr_down(const __grid_constan
         g = fadd(g, fmul(a.down_taps[q], tG[2 * yo + q][xo]));
         m = fadd(m, fmul(a.down_taps[q], tM[2 * yo + q][xo]));
     }
-    const size_t o = static_cast<size_t>(Y - wo.y0) * wo.w + (X - wo.x0);
+    const int o = (Y - wo.y0) * wo.w + (X - wo.x0);
     a.G[c][k + 1][o] = g;
     a.M[c][k + 1][o] = m;
 }
@@ -304,10 +337,10 @@ __global__ void __launch_bounds__(256) k_blend_level(const __grid_constant__ Com
     __shared__ float sG[BMAXC][BS_Y][BS_X];
     __shared__ float sR[BS_Y][BS_X];
     __shared__ int s_cams[kMaxCompCams];
+    __shared__ int s_full[kMaxCompCams];  // tile entirely inside the camera's window
     __shared__ int s_nc;
     __shared__ int s_x0[BT_X], s_y0[BT_Y];
     __shared__ float s_ax[BT_X], s_ay[BT_Y];
-    __shared__ int4 s_ri[BMAXC][BT_Y];
     const int bx = blockIdx.x * BT_X, by = blockIdx.y * BT_Y;
     const int Wk = a.W[k], Hk = a.H[k];
     const bool top = k == a.levels - 1;
@@ -316,8 +349,11 @@ __global__ void __launch_bounds__(256) k_blend_level(const __grid_constant__ Com
         int n = 0;
         for (int q = 0; q < a.ncams; ++q) {
             const Win& w = a.win[q][k];
-            if (w.w > 0 && w.h > 0 && w.x0 < bx + BT_X && w.x0 + w.w > bx && w.y0 < by + BT_Y && w.y0 + w.h > by)
+            if (w.w > 0 && w.h > 0 && w.x0 < bx + BT_X && w.x0 + w.w > bx && w.y0 < by + BT_Y && w.y0 + w.h > by) {
+                s_full[n] = w.x0 <= bx && w.x0 + w.w >= min(bx + BT_X, Wk) && w.y0 <= by &&
+                            w.y0 + w.h >= min(by + BT_Y, Hk);
                 s_cams[n++] = q;
+            }
         }
         s_nc = n;
     }
@@ -354,17 +390,10 @@ __global__ void __launch_bounds__(256) k_blend_level(const __grid_constant__ Com
                 const int cam = s_cams[slot];
                 sG[slot][r][q] = win_at(a.G[cam][k + 1], a.win[cam][k + 1], gx, gy);
             } else {
-                sR[r][q] = Rn[static_cast<size_t>(gy) * W1 + gx];
+                sR[r][q] = Rn[gy * W1 + gx];
             }
         }
     }
-    const bool analytic = k == 0 && a.analytic_masks;
-    if (analytic)
-        for (int i = tid; i < nst * BT_Y; i += blockDim.x) {
-            const int q = i / BT_Y, r = i - q * BT_Y;
-            const int cam = s_cams[q];
-            s_ri[q][r] = load_run_info(a, cam, by + r - a.win[cam][0].y0);
-        }
     __syncthreads();
     for (int p = tid; p < BT_X * BT_Y; p += blockDim.x) {
         const int px = p % BT_X, py = p / BT_X;
@@ -378,31 +407,13 @@ __global__ void __launch_bounds__(256) k_blend_level(const __grid_constant__ Com
             ax = s_ax[px];
             ay = s_ay[py];
         }
-        float sum = 0.0f;
-        float dl[BMAXC];
-        if (analytic)
-            for (int i = 0; i < nc; ++i) {
-                const int cam = s_cams[i];
-                const Win& w = a.win[cam][0];
-                if (!in_win(w, x, y)) continue;
-                const float d = i < BMAXC ? dist_staged(a, s_ri[i][py], cam, y - w.y0, x - w.x0)
-                                          : run_dist(a, cam, y - w.y0, x - w.x0);
-                if (i < BMAXC) dl[i] = d;
-                sum = fadd(sum, d);
-            }
         float acc = 0.0f, ws = 0.0f;
         for (int i = 0; i < nc; ++i) {
             const int cam = s_cams[i];
             const Win& w = a.win[cam][k];
-            if (!in_win(w, x, y)) continue;
-            const size_t o = static_cast<size_t>(y - w.y0) * w.w + (x - w.x0);
-            float wt;
-            if (analytic) {
-                const float d = i < BMAXC ? dl[i] : run_dist(a, cam, y - w.y0, x - w.x0);
-                wt = sum > 0.0f ? __fdiv_rn(d, sum) : d;
-            } else {
-                wt = a.M[cam][k][o];
-            }
+            if (!s_full[i] && !in_win(w, x, y)) continue;
+            const int o = (y - w.y0) * w.w + (x - w.x0);
+            const float wt = a.M[cam][k][o];
             float band = a.G[cam][k][o];
             if (!top) {
                 float up;
@@ -422,7 +433,7 @@ __global__ void __launch_bounds__(256) k_blend_level(const __grid_constant__ Com
         if (!top)
             acc = fadd(acc, bilerp(ax, ay, sR[ya][xa], sR[ya][xa + 1], sR[ya + 1][xa], sR[ya + 1][xa + 1]));
         if (k > 0)
-            a.R[k][static_cast<size_t>(y) * Wk + x] = acc;
+            a.R[k][y * Wk + x] = acc;
         else
             a.out[static_cast<size_t>(y) * Wk + x] = ws > 0.0f ? to_u8(acc) : 0;
     }
@@ -456,8 +467,11 @@ void compose_launch(const ComposeArgs& a, cudaStream_t s) {
     LPB_LAUNCH(k_warp, g0, dim3(32, 8), 0, s, a);
     dim3 g1(cdiv(mh, 8), a.ncams);
     LPB_LAUNCH(k_runs, g1, 256, 0, s, a);
+    dim3 g2(cdiv(mw, MK_TX), cdiv(mh, MK_TY), a.ncams);
+    LPB_LAUNCH(k_mask0, g2, 256, 0, s, a);
     blend_launch(a, s);
 }
+
 
 // ---------------------------------------------------------------------------
 // stage-isolated primitives (full-canvas, channels)
