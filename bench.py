@@ -44,7 +44,94 @@ CONFIGS = {
                  workload="cfg2: 2-camera 1920x1080, per-frame re-registration"),
     "cfg1": dict(ncams=2, w=640, h=480, refresh=1,
                  workload="cfg1: 2-camera 640x480 planted pair, full pipeline"),
+    "cfg5": dict(ncams=2, w=1920, h=1080, refresh=1, streams=64,
+                 workload="cfg5: 64 independent 1920x1080 2-camera streams, per-frame "
+                          "re-registration, sharded contiguously across the GPUs"),
 }
+
+
+def run_streams(args, cfgd, lp, world, rank, local, dist):
+    """Config 5: the rank's contiguous share of 64 independent 2-camera streams
+    (one rig each), driven by host threads so the rigs' per-frame estimator
+    synchronisations overlap. A step = one frame of every stream of the job."""
+    import threading
+
+    import torch
+
+    from paper_1810_03988_b200 import Rig, kernel_launches
+    from paper_1810_03988_b200.shard import RankResult, aggregate_fps, gather_results, shard_streams
+    mine = shard_streams(cfgd["streams"], world, rank)
+    p = lp.default_params()
+    p.seed = p.matching.seed = 42
+    p.homography_refresh = cfgd["refresh"]
+    w, h = cfgd["w"], cfgd["h"]
+    rigs, inputs, panos = [], [], []
+    for s in mine:
+        sets, _ = make_frame_sets(2, w, h, 1, seed=42 + s)
+        inputs.append([torch.from_numpy(c).cuda() for c in sets[0]])
+        rig = Rig(lp, 2, w, h, p)
+        rigs.append(rig)
+        panos.append(torch.empty(rig.panorama_capacity(), dtype=torch.uint8, device="cuda"))
+    nthreads = min(len(rigs), 16)
+    groups = [list(range(i, len(rigs), nthreads)) for i in range(nthreads)]
+
+    def run(steps, base):
+        errs = []
+
+        def worker(ids):
+            try:
+                for t in range(steps):
+                    for i in ids:
+                        tk = rigs[i].submit([x.data_ptr() for x in inputs[i]], base + t,
+                                            panos[i].data_ptr(), panos[i].numel())
+                        rigs[i].wait(tk)
+            except Exception as e:  # surfaced after join
+                errs.append(e)
+        ths = [threading.Thread(target=worker, args=(g,)) for g in groups]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        if errs:
+            raise errs[0]
+
+    run(args.warmup, 0)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clocks = Clocks(local)
+    n0 = kernel_launches()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    run(args.steps, 1000)
+    torch.cuda.synchronize()
+    el_ms = (time.perf_counter() - t0) * 1e3
+    clk = clocks.stop()
+    launches = kernel_launches() - n0
+    csum = sum(int(pb[:1 << 20].to(torch.int64).sum().item()) for pb in panos)
+    ms_max, frames, checksums = gather_results(RankResult(args.steps * len(rigs), el_ms, csum),
+                                               torch.device("cuda", local))
+    if rank == 0:
+        line = {"metric": METRIC, "value": aggregate_fps(frames, ms_max), "unit": "frames/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "u8/f32/f64", "data": "synthetic",
+                "config": {"workload": cfgd["workload"], "streams": cfgd["streams"],
+                           "streams_per_gpu": len(mine), "host_threads_per_gpu": nthreads,
+                           "cameras": 2, "width": w, "height": h,
+                           "l2": "64 distinct streams (265 MB of frames) > 126 MB L2",
+                           "parallelism": f"shards x{world} (contiguous stream blocks, no data-path collective)"},
+                "timing": "wall clock between device-wide synchronisations, max over ranks",
+                "gpu_launches": int(launches), "clocks": clk, "rank_checksums": checksums,
+                "roofline": None, "cpu_baseline": None, "e2e": None}
+        s = json.dumps(line)
+        print(s)
+        if args.out:
+            open(args.out, "w").write(s + "\n")
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
 
 
 def texture(w, h, seed, sigma=1.5):
@@ -238,8 +325,11 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_1810_03988_b200 import Lorb, Rig, abi, frame_out, kernel_launches, load
+    from paper_1810_03988_b200.shard import RankResult, aggregate_fps, gather_results
     lib = load()
     lp = Lorb(local)
+    if args.config == "cfg5":
+        return run_streams(args, cfgd, lp, world, rank, local, dist)
     ncams, w, h = cfgd["ncams"], cfgd["w"], cfgd["h"]
     p = lp.default_params()
     p.seed = p.matching.seed = 42
@@ -280,21 +370,13 @@ def main():
     clk = clocks.stop()
     launches = kernel_launches() - n0
     ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = world * args.steps / (ms_max / 1e3)
-
-    # panorama checksum gathered to rank 0 (the only other collective)
+    # the only collectives: MAX of device time, SUM of frames, gather of
+    # panorama checksums (paper_1810_03988_b200.shard)
     pano = dpano[:canvas[0] * canvas[1]]
-    csum = torch.tensor([int(pano.to(torch.int64).sum().item())], dtype=torch.int64, device="cuda")
-    if dist is not None:
-        allc = [torch.zeros_like(csum) for _ in range(world)]
-        dist.all_gather(allc, csum)
-        checksums = [int(x.item()) for x in allc]
-    else:
-        checksums = [int(csum.item())]
+    csum = int(pano.to(torch.int64).sum().item())
+    ms_max, total_frames, checksums = gather_results(RankResult(args.steps, ms, csum),
+                                                     torch.device("cuda", local))
+    value = aggregate_fps(total_frames, ms_max)
 
     # ---- per-kernel profile pass (same workload; events around every launch)
     roofline = None
