@@ -103,36 +103,56 @@ __device__ __forceinline__ float dist_staged(const ComposeArgs& a, const int4& r
 }
 
 // ---------------------------------------------------------------------------
+constexpr int WP_ROWS = 4;  // rows per thread: independent FP64 chains and gathers in flight
+
 __global__ void __launch_bounds__(256) k_warp(const __grid_constant__ ComposeArgs a) {
     const int c = blockIdx.z;
     const Win w = a.win[c][0];
-    const int lx = blockIdx.x * 32 + threadIdx.x, ly = blockIdx.y * blockDim.y + threadIdx.y;
-    const bool inb = lx < w.w && ly < w.h;
-    bool covered = false;
-    float v = 0.0f;
-    if (inb) {
-        const double* hi = a.hinv[c];
-        const DevImage im = a.src[c];
-        const double X = static_cast<double>(w.x0 + lx + a.origin_x), Y = static_cast<double>(w.y0 + ly + a.origin_y);
-        const double wd = hi[6] * X + hi[7] * Y + hi[8];
-        const double sx = (hi[0] * X + hi[1] * Y + hi[2]) / wd;
-        const double sy = (hi[3] * X + hi[4] * Y + hi[5]) / wd;
-        if (!(sx < 0.0 || sx > im.w - 1 || sy < 0.0 || sy > im.h - 1)) {
-            const int x0 = static_cast<int>(sx), y0 = static_cast<int>(sy);
-            const double ax = sx - x0, ay = sy - y0;
+    const int lx = blockIdx.x * 32 + threadIdx.x;
+    const int ly0 = blockIdx.y * (8 * WP_ROWS) + threadIdx.y;
+    const double* hi = a.hinv[c];
+    const DevImage im = a.src[c];
+    const double X = static_cast<double>(w.x0 + lx + a.origin_x);
+    const double xw = hi[6] * X, xn = hi[0] * X, xm = hi[3] * X;
+    double sx[WP_ROWS], sy[WP_ROWS];
+    bool cov[WP_ROWS];
+#pragma unroll
+    for (int j = 0; j < WP_ROWS; ++j) {
+        const int ly = ly0 + 8 * j;
+        const double Y = static_cast<double>(w.y0 + ly + a.origin_y);
+        // same operation order as Homography::apply (homography.hpp:30-33)
+        const double wd = xw + hi[7] * Y + hi[8];
+        sx[j] = (xn + hi[1] * Y + hi[2]) / wd;
+        sy[j] = (xm + hi[4] * Y + hi[5]) / wd;
+        cov[j] = lx < w.w && ly < w.h && !(sx[j] < 0.0 || sx[j] > im.w - 1 || sy[j] < 0.0 || sy[j] > im.h - 1);
+    }
+    uint32_t q[WP_ROWS];  // the four taps packed as bytes
+#pragma unroll
+    for (int j = 0; j < WP_ROWS; ++j) {
+        q[j] = 0;
+        if (cov[j]) {
+            const int x0 = static_cast<int>(sx[j]), y0 = static_cast<int>(sy[j]);
             const int x1 = min(x0 + 1, im.w - 1), y1 = min(y0 + 1, im.h - 1);
             const uint8_t* r0 = im.p + static_cast<size_t>(y0) * im.w;
             const uint8_t* r1 = im.p + static_cast<size_t>(y1) * im.w;
-            const double v00 = __ldg(r0 + x0), v10 = __ldg(r0 + x1);
-            const double v01 = __ldg(r1 + x0), v11 = __ldg(r1 + x1);
-            v = __double2float_rn((1 - ay) * ((1 - ax) * v00 + ax * v10) + ay * ((1 - ax) * v01 + ax * v11));
-            covered = true;
+            q[j] = static_cast<uint32_t>(__ldg(r0 + x0)) | (static_cast<uint32_t>(__ldg(r0 + x1)) << 8) |
+                   (static_cast<uint32_t>(__ldg(r1 + x0)) << 16) | (static_cast<uint32_t>(__ldg(r1 + x1)) << 24);
         }
-        a.G[c][0][static_cast<size_t>(ly) * w.w + lx] = v;
     }
-    const unsigned bits = __ballot_sync(0xffffffffu, covered);
-    if (threadIdx.x == 0 && ly < w.h && blockIdx.x * 32 < w.w)
-        a.cov[c][static_cast<size_t>(ly) * a.cov_words[c] + blockIdx.x] = bits;
+#pragma unroll
+    for (int j = 0; j < WP_ROWS; ++j) {
+        const int ly = ly0 + 8 * j;
+        float v = 0.0f;
+        if (cov[j]) {
+            const int x0 = static_cast<int>(sx[j]), y0 = static_cast<int>(sy[j]);
+            const double ax = sx[j] - x0, ay = sy[j] - y0;
+            const double v00 = q[j] & 0xFF, v10 = (q[j] >> 8) & 0xFF, v01 = (q[j] >> 16) & 0xFF, v11 = q[j] >> 24;
+            v = __double2float_rn((1 - ay) * ((1 - ax) * v00 + ax * v10) + ay * ((1 - ax) * v01 + ax * v11));
+        }
+        if (lx < w.w && ly < w.h) a.G[c][0][ly * w.w + lx] = v;
+        const unsigned bits = __ballot_sync(0xffffffffu, cov[j]);
+        if (threadIdx.x == 0 && ly < w.h && blockIdx.x * 32 < w.w) a.cov[c][ly * a.cov_words[c] + blockIdx.x] = bits;
+    }
 }
 
 // warp per (camera, window row): covered runs from the coverage bit words
@@ -206,7 +226,7 @@ __global__ void __launch_bounds__(256) k_runs(const __grid_constant__ ComposeArg
 // distance to the pixel's coverage-run ends, divided by the camera-ordered
 // sum over every camera covering the pixel. Runs are staged per (camera,
 // row) in canvas coordinates, so no window tests are needed.
-constexpr int MK_TX = 64, MK_TY = 8;
+constexpr int MK_TX = 64, MK_TY = 32;  // 8 pixels per thread amortise the run staging
 
 __global__ void __launch_bounds__(256) k_mask0(const __grid_constant__ ComposeArgs a) {
     __shared__ int s_cams[kMaxCompCams];
@@ -395,23 +415,39 @@ __global__ void __launch_bounds__(256) k_blend_level(const __grid_constant__ Com
         }
     }
     __syncthreads();
-    for (int p = tid; p < BT_X * BT_Y; p += blockDim.x) {
-        const int px = p % BT_X, py = p / BT_X;
-        const int x = bx + px, y = by + py;
-        if (x >= Wk || y >= Hk) continue;
-        int xa = 0, ya = 0;
-        float ax = 0.0f, ay = 0.0f;
+    // thread = one column of the tile, BT_Y / 4 rows: column quantities
+    // (upsample x tap and weight, per-camera horizontal window test) hoisted
+    const int px = tid & (BT_X - 1), pyb = tid / BT_X;
+    const int x = bx + px;
+    if (x >= Wk) return;
+    int xa = 0;
+    float ax = 0.0f;
+    if (!top) {
+        xa = s_x0[px] - lx0;
+        ax = s_ax[px];
+    }
+    unsigned colmask = 0;  // cameras whose window holds column x
+    for (int i = 0; i < nc; ++i) {
+        const Win& w = a.win[s_cams[i]][k];
+        if (s_full[i] || (x >= w.x0 && x < w.x0 + w.w)) colmask |= 1u << i;
+    }
+#pragma unroll
+    for (int j = 0; j < BT_Y / (256 / BT_X); ++j) {
+        const int py = pyb + j * (256 / BT_X);
+        const int y = by + py;
+        if (y >= Hk) break;
+        int ya = 0;
+        float ay = 0.0f;
         if (!top) {
-            xa = s_x0[px] - lx0;
             ya = s_y0[py] - ly0;
-            ax = s_ax[px];
             ay = s_ay[py];
         }
         float acc = 0.0f, ws = 0.0f;
         for (int i = 0; i < nc; ++i) {
+            if (!((colmask >> i) & 1u)) continue;
             const int cam = s_cams[i];
             const Win& w = a.win[cam][k];
-            if (!s_full[i] && !in_win(w, x, y)) continue;
+            if (!s_full[i] && (y < w.y0 || y >= w.y0 + w.h)) continue;
             const int o = (y - w.y0) * w.w + (x - w.x0);
             const float wt = a.M[cam][k][o];
             float band = a.G[cam][k][o];
@@ -463,7 +499,7 @@ void compose_launch(const ComposeArgs& a, cudaStream_t s) {
         mh = std::max(mh, a.win[c][0].h);
     }
     LPB_CUDA(cudaMemsetAsync(a.runs_used, 0, sizeof(int), s));
-    dim3 g0(cdiv(mw, 32), cdiv(mh, 8), a.ncams);
+    dim3 g0(cdiv(mw, 32), cdiv(mh, 8 * WP_ROWS), a.ncams);
     LPB_LAUNCH(k_warp, g0, dim3(32, 8), 0, s, a);
     dim3 g1(cdiv(mh, 8), a.ncams);
     LPB_LAUNCH(k_runs, g1, 256, 0, s, a);
