@@ -50,7 +50,7 @@ constexpr int NMS_W = TW + 2;                          // 34
 // R = ceil(3*1.0) = 3, arc 9): tile geometry and the arc test fold to constants.
 // 0: runtime values from ExtractArgs.
 template <int RT, int ARCT>
-__global__ void __launch_bounds__(256) k_detect(ExtractArgs a) {
+__global__ void __launch_bounds__(256, 4) k_detect(ExtractArgs a) {
     // gradients kept as the exact doubles the reference forms,
     // (double(I(x+1)) - I(x-1)) / 2.0 (lorb.hpp:239-240), sized for the instance's radius
     constexpr int GM = RT > 0 ? TW + 2 + 2 * RT : GRAD_MAX;
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256) k_detect(ExtractArgs a) {
         // gradient-local centre of this pixel
         int gcx = lx - 1 + R + 1, gcy = ly - 1 + R + 1;
         double sa = 0.0, sb = 0.0, sc = 0.0;
-#pragma unroll
+#pragma unroll 1
         for (int v = -R; v <= R; ++v) {
             const double* rx = s_gx + (gcy + v) * gw + gcx;
             const double* ry = s_gy + (gcy + v) * gw + gcx;
