@@ -50,13 +50,13 @@ constexpr int NMS_W = TW + 2;                          // 34
 // R = ceil(3*1.0) = 3, arc 9): tile geometry and the arc test fold to constants.
 // 0: runtime values from ExtractArgs.
 template <int RT, int ARCT>
-__global__ void __launch_bounds__(256, 4) k_detect(ExtractArgs a) {
-    // gradients kept as the exact doubles the reference forms,
-    // (double(I(x+1)) - I(x-1)) / 2.0 (lorb.hpp:239-240), sized for the instance's radius
+__global__ void __launch_bounds__(256) k_detect(ExtractArgs a) {
+    // integer central differences; the Harris loop forms the reference's exact
+    // double (double(I(x+1)) - I(x-1)) / 2.0 (lorb.hpp:239-240) per tap
     constexpr int GM = RT > 0 ? TW + 2 + 2 * RT : GRAD_MAX;
     __shared__ uint8_t s_img[IMG_MAX * IMG_MAX];
-    __shared__ double s_gx[GM * GM];
-    __shared__ double s_gy[GM * GM];
+    __shared__ short s_gx[GM * GM];
+    __shared__ short s_gy[GM * GM];
     __shared__ float s_resp[NMS_W * NMS_W];
     __shared__ short s_cand[NMS_W * NMS_W];
     __shared__ double s_w[(2 * kMaxHarrisR + 1) * (2 * kMaxHarrisR + 1)];
@@ -98,8 +98,8 @@ __global__ void __launch_bounds__(256, 4) k_detect(ExtractArgs a) {
     for (int i = tid; i < gw * gw; i += blockDim.x) {
         int ly = i / gw, lx = i - ly * gw;
         int ix = lx + goff, iy = ly + goff;
-        s_gx[i] = (static_cast<double>(s_img[iy * iw + ix + 1]) - s_img[iy * iw + ix - 1]) / 2.0;
-        s_gy[i] = (static_cast<double>(s_img[(iy + 1) * iw + ix]) - s_img[(iy - 1) * iw + ix]) / 2.0;
+        s_gx[i] = static_cast<short>(int(s_img[iy * iw + ix + 1]) - int(s_img[iy * iw + ix - 1]));
+        s_gy[i] = static_cast<short>(int(s_img[(iy + 1) * iw + ix]) - int(s_img[(iy - 1) * iw + ix]));
     }
 
     // FAST-9 on the tile + 1-px ring, restricted to the scan area
@@ -148,15 +148,13 @@ __global__ void __launch_bounds__(256, 4) k_detect(ExtractArgs a) {
         // gradient-local centre of this pixel
         int gcx = lx - 1 + R + 1, gcy = ly - 1 + R + 1;
         double sa = 0.0, sb = 0.0, sc = 0.0;
-#pragma unroll 1
         for (int v = -R; v <= R; ++v) {
-            const double* rx = s_gx + (gcy + v) * gw + gcx;
-            const double* ry = s_gy + (gcy + v) * gw + gcx;
+            const short* rx = s_gx + (gcy + v) * gw + gcx;
+            const short* ry = s_gy + (gcy + v) * gw + gcx;
             const double* wr = s_w + (v + R) * K + R;
-#pragma unroll
             for (int u = -R; u <= R; ++u) {
-                const double ix = rx[u];
-                const double iy = ry[u];
+                const double ix = static_cast<double>(rx[u]) / 2.0;
+                const double iy = static_cast<double>(ry[u]) / 2.0;
                 const double wt = wr[u];
                 sa = dadd(sa, dmul(dmul(wt, ix), ix));
                 sb = dadd(sb, dmul(dmul(wt, iy), iy));
