@@ -169,7 +169,17 @@ def make_frame_sets(ncams, w, h, nsets, seed=42, overlap=0.25):
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """SM clock / throttle-reason sampler running during the timed region.
+
+    NVML (nvidia_ml_py) polled from a thread every 2 ms, so even a timed
+    region of a few tens of milliseconds carries samples; nvidia-smi -lms 100
+    is the fallback when NVML is unavailable."""
+
+    def __new__(cls, index):
+        try:
+            return _NvmlClocks(index)
+        except Exception:
+            return super().__new__(cls)
 
     def __init__(self, index):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
@@ -204,6 +214,63 @@ class Clocks:
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
                 "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded)}
+
+
+class _NvmlClocks:
+    REASONS = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown")]
+
+    def __init__(self, index):
+        import threading
+
+        import pynvml as N
+        N.nvmlInit()
+        self.N = N
+        h = None
+        try:  # map the torch device to its NVML handle through the UUID
+            import torch
+            u = str(torch.cuda.get_device_properties(index).uuid)
+            h = N.nvmlDeviceGetHandleByUUID(u if u.startswith("GPU-") else "GPU-" + u)
+        except Exception:
+            h = N.nvmlDeviceGetHandleByIndex(index)
+        self.h = h
+        self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+        self.rows = []
+        self.stop_ev = threading.Event()
+        self.sample()
+        self.th = threading.Thread(target=self.loop, daemon=True)
+        self.th.start()
+
+    def sample(self):
+        N = self.N
+        sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+        rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        util = N.nvmlDeviceGetUtilizationRates(self.h).gpu
+        self.rows.append((float(sm), int(rs), int(util)))
+
+    def loop(self):
+        while not self.stop_ev.wait(0.002):
+            self.sample()
+
+    def stop(self):
+        self.stop_ev.set()
+        self.th.join()
+        self.sample()
+        N = self.N
+        rows = self.rows
+        loaded = [r for r in rows if r[2] > 0] or rows
+        reasons = sorted({name for name, attr in self.REASONS for r in rows
+                          if r[1] & getattr(N, attr, 0)})
+        try:
+            N.nvmlShutdown()
+        except Exception:
+            pass
+        return {"sm_mhz": float(np.median([r[0] for r in loaded])), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded),
+                "sampler": "NVML every 2 ms"}
 
 
 def measured_peak_hbm():
@@ -301,8 +368,8 @@ def run_reference(args, cfgd):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")

@@ -229,9 +229,17 @@ static void validate_ext(const lp_extraction_config& c) {  // lorb.hpp:82-89
 // Constant per-configuration tables for the extractor.
 struct ExtractTables {
     DBuf harris_w, taps, pairs;
+    std::vector<double> hw;
     int harris_r = 0, blur_r = 0;
+    // the weights again in the kernel's parameter bank (k_detect9 reads them
+    // as constant operands)
+    void fill(ExtractArgs& a) const {
+        a.harris_w = harris_w.as<double>();
+        a.harris_r = harris_r;
+        for (size_t i = 0; i < 49; ++i) a.hw[i] = i < hw.size() ? hw[i] : 0.0;
+    }
     ExtractTables(const lp_extraction_config& c, const std::vector<lp_pair>& pat, cudaStream_t s) {
-        auto hw = host::harris_weights(c.harris_sigma, &harris_r);
+        hw = host::harris_weights(c.harris_sigma, &harris_r);
         if (harris_r > kMaxHarrisR) throw Status(LP_BAD_PARAMS, "harris_sigma too large for the device tile");
         auto tp = host::gaussian_kernel(c.brief_blur_sigma);
         blur_r = static_cast<int>(tp.size() / 2);
@@ -246,9 +254,9 @@ struct ExtractTables {
 static std::vector<DevRegion> make_dev_regions(const std::vector<lp_region>& regs,
                                                const std::vector<int>& img_of,
                                                const std::vector<int>& slot_of, const int* w,
-                                               const int* h, int* total_tiles) {
+                                               const int* h, int* max_tiles) {
     std::vector<DevRegion> out;
-    int base = 0;
+    int mt = 0;
     for (size_t i = 0; i < regs.size(); ++i) {
         const lp_region& r = regs[i];
         const int im = img_of[i];
@@ -264,13 +272,13 @@ static std::vector<DevRegion> make_dev_regions(const std::vector<lp_region>& reg
         d.ry0 = r.y0;
         d.rx1 = r.x1;
         d.ry1 = r.y1;
-        d.tiles_x = cdiv(d.x1 - d.x0, kDetTile);
-        d.tile_base = base;
+        d.tiles_x = cdiv(d.x1 - d.x0, kDetTileX);
+        d.ntiles = d.tiles_x * cdiv(d.y1 - d.y0, kDetTileY);
         d.out_slot = slot_of[i];
-        base += d.tiles_x * cdiv(d.y1 - d.y0, kDetTile);
+        mt = std::max(mt, d.ntiles);
         out.push_back(d);
     }
-    *total_tiles = base;
+    *max_tiles = mt;
     return out;
 }
 
@@ -585,10 +593,9 @@ lp_status lp_extract_features(lp_ctx* ctx, const uint8_t* img, int w, int h, int
         ExtractArgs a{};
         a.regions = dr.as<DevRegion>();
         a.nregions = nreg;
-        a.total_tiles = tiles;
+        a.max_tiles = tiles;
         a.images = dims.as<DevImage>();
-        a.harris_w = T.harris_w.as<double>();
-        a.harris_r = T.harris_r;
+        T.fill(a);
         a.alpha = cfg->harris_alpha;
         a.threshold = cfg->harris_threshold;
         a.fast_t = static_cast<uint8_t>(cfg->fast_threshold);

@@ -39,42 +39,74 @@ __constant__ int c_ring_dx[16] = {0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3, -3, -3,
 __constant__ int c_ring_dy[16] = {-3, -3, -2, -1, 0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3};
 
 // ---------------------------------------------------------------------------
-// k_detect
-constexpr int TW = kDetTile;
+// k_detect<RT, ARCT>: generic instance (any Harris radius <= kMaxHarrisR, any
+// arc), one CTA per kDetTileX x kDetTileY output tile, grid (tiles, regions)
+constexpr int TX = kDetTileX, TY = kDetTileY;
+constexpr int NX = TX + 2, NY = TY + 2;                 // response grid: tile + 1-px ring
 constexpr int HALO_MAX = kMaxHarrisR + 2;              // harris R + gradient 1 + NMS 1
-constexpr int IMG_MAX = TW + 2 * HALO_MAX;             // 48
-constexpr int GRAD_MAX = TW + 2 + 2 * kMaxHarrisR;     // 46
-constexpr int NMS_W = TW + 2;                          // 34
+constexpr int IMG_MAX_X = TX + 2 * HALO_MAX, IMG_MAX_Y = TY + 2 * HALO_MAX;
+constexpr int GRAD_MAX_X = TX + 2 + 2 * kMaxHarrisR, GRAD_MAX_Y = TY + 2 + 2 * kMaxHarrisR;
 
-// RT / ARCT > 0: compile-time Harris radius / FAST arc (the default config,
-// R = ceil(3*1.0) = 3, arc 9): tile geometry and the arc test fold to constants.
-// 0: runtime values from ExtractArgs.
+// survivors of the 3x3 NMS -> per-region key list (ballot-aggregated
+// atomics) and the first radix digit histogram of k_topn
+__device__ __forceinline__ void emit_survivor(const ExtractArgs& a, int ri, bool keep, uint64_t key) {
+    const int lane = threadIdx.x & 31;
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (!m) return;
+    const int leader = __ffs(m) - 1;
+    unsigned pos = 0;
+    if (lane == leader) pos = atomicAdd(&a.surv_count[ri], static_cast<unsigned>(__popc(m)));
+    pos = __shfl_sync(0xffffffffu, pos, leader);
+    if (keep) {
+        const unsigned slot = pos + __popc(m & ((1u << lane) - 1u));
+        if (slot < static_cast<unsigned>(a.surv_cap))
+            a.surv[static_cast<size_t>(ri) * a.surv_cap + slot] = key;
+        else
+            dev_fail(a.status, LP_CAPACITY_OVERFLOW);
+        // first radix digit of k_topn: top 12 key bits (sign, exponent, 3 mantissa bits)
+        atomicAdd(&a.hist[static_cast<size_t>(ri) * kTopnHistBins + (key >> 52)], 1u);
+    }
+}
+
+// 3x3 NMS of one candidate on the response grid (lorb.hpp:254-288): NaN marks
+// "not a thresholded candidate"; exact ties go to the smaller (y, x)
+__device__ __forceinline__ bool nms_wins(const float* resp, int i, float r) {
+    bool keep = true;
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx) {
+            if (dx == 0 && dy == 0) continue;
+            const float o = resp[i + dy * NX + dx];
+            if (o > r || (o == r && (dy < 0 || (dy == 0 && dx < 0)))) keep = false;
+        }
+    return keep;
+}
+
 template <int RT, int ARCT>
 __global__ void __launch_bounds__(256) k_detect(ExtractArgs a) {
     // integer central differences; the Harris loop forms the reference's exact
     // double (double(I(x+1)) - I(x-1)) / 2.0 (lorb.hpp:239-240) per tap
-    constexpr int GM = RT > 0 ? TW + 2 + 2 * RT : GRAD_MAX;
-    __shared__ uint8_t s_img[IMG_MAX * IMG_MAX];
-    __shared__ short s_gx[GM * GM];
-    __shared__ short s_gy[GM * GM];
-    __shared__ float s_resp[NMS_W * NMS_W];
-    __shared__ short s_cand[NMS_W * NMS_W];
+    __shared__ uint8_t s_img[IMG_MAX_X * IMG_MAX_Y];
+    __shared__ short s_gx[GRAD_MAX_X * GRAD_MAX_Y];
+    __shared__ short s_gy[GRAD_MAX_X * GRAD_MAX_Y];
+    __shared__ float s_resp[NX * NY];
+    __shared__ short s_cand[NX * NY];
     __shared__ double s_w[(2 * kMaxHarrisR + 1) * (2 * kMaxHarrisR + 1)];
     __shared__ int s_ncand;
 
-    const int b = blockIdx.x;
-    int ri = 0;
-    while (ri + 1 < a.nregions && a.regions[ri + 1].tile_base <= b) ++ri;
+    const int ri = blockIdx.y;
     const DevRegion rg = a.regions[ri];
+    const int t = blockIdx.x;
+    if (t >= rg.ntiles) return;
     const DevImage im = a.images[rg.img];
-    const int t = b - rg.tile_base;
-    const int ox = rg.x0 + (t % rg.tiles_x) * TW;
-    const int oy = rg.y0 + (t / rg.tiles_x) * TW;
+    const int ox = rg.x0 + (t % rg.tiles_x) * TX;
+    const int oy = rg.y0 + (t / rg.tiles_x) * TY;
     const int R = RT > 0 ? RT : a.harris_r;
     const int arc = ARCT > 0 ? ARCT : a.fast_arc;
     const int halo = (R + 1 > 3 ? R + 1 : 3) + 1;
-    const int iw = TW + 2 * halo;
-    const int gw = TW + 2 + 2 * R;
+    const int iw = TX + 2 * halo, ih = TY + 2 * halo;
+    const int gw = TX + 2 + 2 * R, gh = TY + 2 + 2 * R;
     const int tid = threadIdx.x;
 
     const int K = 2 * R + 1;
@@ -84,43 +116,31 @@ __global__ void __launch_bounds__(256) k_detect(ExtractArgs a) {
     // stage the u8 tile + halo (clamped coordinates; clamped texels are never
     // consumed by a valid test).
     const int gx0 = ox - halo, gy0 = oy - halo;
-    for (int i = tid; i < iw * iw; i += blockDim.x) {
+    for (int i = tid; i < iw * ih; i += blockDim.x) {
         int ly = i / iw, lx = i - ly * iw;
         int gx = min(max(gx0 + lx, 0), im.w - 1);
         int gy = min(max(gy0 + ly, 0), im.h - 1);
         s_img[ly * iw + lx] = __ldg(im.p + static_cast<size_t>(gy) * im.w + gx);
     }
-    for (int i = tid; i < NMS_W * NMS_W; i += blockDim.x) s_resp[i] = __int_as_float(0x7fc00000);
+    for (int i = tid; i < NX * NY; i += blockDim.x) s_resp[i] = __int_as_float(0x7fc00000);
     __syncthreads();
 
     // integer central differences over the Harris window area
     const int goff = halo - 1 - R;  // gradient (0,0) sits at image-local (goff, goff)
-    for (int i = tid; i < gw * gw; i += blockDim.x) {
+    for (int i = tid; i < gw * gh; i += blockDim.x) {
         int ly = i / gw, lx = i - ly * gw;
         int ix = lx + goff, iy = ly + goff;
         s_gx[i] = static_cast<short>(int(s_img[iy * iw + ix + 1]) - int(s_img[iy * iw + ix - 1]));
         s_gy[i] = static_cast<short>(int(s_img[(iy + 1) * iw + ix]) - int(s_img[(iy - 1) * iw + ix]));
     }
 
-    // FAST-9 on the tile + 1-px ring, restricted to the scan area
-    for (int i = tid; i < NMS_W * NMS_W; i += blockDim.x) {
-        int ly = i / NMS_W, lx = i - ly * NMS_W;
+    // FAST on the tile + 1-px ring, restricted to the scan area
+    for (int i = tid; i < NX * NY; i += blockDim.x) {
+        int ly = i / NX, lx = i - ly * NX;
         int px = ox - 1 + lx, py = oy - 1 + ly;
         if (px < rg.x0 || px >= rg.x1 || py < rg.y0 || py >= rg.y1) continue;
         int cx = px - gx0, cy = py - gy0;
         int c = s_img[cy * iw + cx];
-        {
-            // necessary condition for any arc >= 9 of the 16-ring: two circularly
-            // adjacent compass points (ring 0/4/8/12) pass the same test, since
-            // 9 consecutive ring positions always hold two consecutive multiples of 4
-            const int v0 = s_img[(cy - 3) * iw + cx], v4 = s_img[cy * iw + cx + 3];
-            const int v8 = s_img[(cy + 3) * iw + cx], v12 = s_img[cy * iw + cx - 3];
-            const int hi = c + a.fast_t, lo = c - a.fast_t;
-            const unsigned cb = (v0 > hi) | ((v4 > hi) << 1) | ((v8 > hi) << 2) | ((v12 > hi) << 3);
-            const unsigned cd = (v0 < lo) | ((v4 < lo) << 1) | ((v8 < lo) << 2) | ((v12 < lo) << 3);
-            auto adjacent = [](unsigned m) { return (m & ((m >> 1) | (m << 3)) & 0xFu) != 0u; };
-            if (!adjacent(cb) && !adjacent(cd)) continue;
-        }
         unsigned br = 0, dk = 0;
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
@@ -144,9 +164,9 @@ __global__ void __launch_bounds__(256) k_detect(ExtractArgs a) {
     const double alpha = static_cast<double>(a.alpha);
     for (int j = tid; j < nc; j += blockDim.x) {
         int i = s_cand[j];
-        int ly = i / NMS_W, lx = i - ly * NMS_W;
+        int ly = i / NX, lx = i - ly * NX;
         // gradient-local centre of this pixel
-        int gcx = lx - 1 + R + 1, gcy = ly - 1 + R + 1;
+        int gcx = lx + R, gcy = ly + R;
         double sa = 0.0, sb = 0.0, sc = 0.0;
         for (int v = -R; v <= R; ++v) {
             const short* rx = s_gx + (gcy + v) * gw + gcx;
@@ -169,43 +189,240 @@ __global__ void __launch_bounds__(256) k_detect(ExtractArgs a) {
     __syncthreads();
 
     // 3x3 NMS among thresholded candidates; survivors -> per-region key list
-    const int lane = tid & 31;
-    for (int base = 0; base < TW * TW; base += blockDim.x) {
-        int i = base + tid;
+    for (int base = 0; base < TX * TY; base += blockDim.x) {
+        const int i = base + tid;
         bool keep = false;
         uint64_t key = 0;
-        if (i < TW * TW) {
-            int ly = i / TW + 1, lx = i % TW + 1;
-            float r = s_resp[ly * NMS_W + lx];
+        if (i < TX * TY) {
+            const int ly = i / TX + 1, lx = i % TX + 1;
+            const float r = s_resp[ly * NX + lx];
             if (r == r) {
-                keep = true;
-#pragma unroll
-                for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-                    for (int dx = -1; dx <= 1; ++dx) {
-                        if (dx == 0 && dy == 0) continue;
-                        float o = s_resp[(ly + dy) * NMS_W + lx + dx];
-                        if (o > r || (o == r && (dy < 0 || (dy == 0 && dx < 0)))) keep = false;
-                    }
+                keep = nms_wins(s_resp, ly * NX + lx, r);
                 key = kp_key(r, ox + lx - 1, oy + ly - 1);
             }
         }
-        unsigned m = __ballot_sync(0xffffffffu, keep);
-        if (m) {
-            int leader = __ffs(m) - 1;
-            unsigned pos = 0;
-            if (lane == leader) pos = atomicAdd(&a.surv_count[ri], static_cast<unsigned>(__popc(m)));
-            pos = __shfl_sync(0xffffffffu, pos, leader);
-            if (keep) {
-                unsigned slot = pos + __popc(m & ((1u << lane) - 1u));
-                if (slot < static_cast<unsigned>(a.surv_cap))
-                    a.surv[static_cast<size_t>(ri) * a.surv_cap + slot] = key;
+        emit_survivor(a, ri, keep, key);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_detect9: the default configuration (Harris radius 3, FAST arc 9).
+//  * the tile is staged as 32-bit words aligned to global 4-pixel groups;
+//  * FAST tests four pixels per thread in SIMD-within-a-register form: per
+//    ring position one byte-permute builds the four ring values, bytewise
+//    unsigned compares against saturated c+t / c-t leave one flag per byte
+//    (msb), and the arc-9 test is AND-of-3 (x2) + OR over the 16 rotations;
+//  * Harris folds the reference's /2.0 of both gradients into one exact *0.25
+//    per sum (binary scaling commutes with every rounding on the way), reads
+//    packed (gx, gy) shorts and takes the 49 window weights from the
+//    parameter bank, fully unrolled in the reference's v-then-u order;
+//  * NMS runs over the candidate list only.
+namespace d9 {
+constexpr int FW = (NX + 6) / 4;   // FAST words per row: 4 px each, global-aligned
+constexpr int SWW = FW + 2;        // staged words per row (one each side for the ring)
+constexpr int SB = 4 * SWW;        // staged row pitch in bytes
+constexpr int SH = TY + 10;        // staged rows oy-5 .. oy+TY+4
+constexpr int GX = TX + 8, GY = TY + 8;  // gradient grid: ox-4 .. ox+TX+3, oy-4 .. oy+TY+3
+constexpr int NTASK = NY * FW;
+__device__ constexpr int ring_dx(int k) {
+    constexpr int t[16] = {0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3, -3, -3, -2, -1};
+    return t[k];
+}
+__device__ constexpr int ring_dy(int k) {
+    constexpr int t[16] = {-3, -3, -2, -1, 0, 1, 2, 3, 3, 3, 2, 1, 0, -1, -2, -3};
+    return t[k];
+}
+
+// msb of byte b = (x_b > y_b), unsigned; other bits are don't-care
+__device__ __forceinline__ uint32_t gt_u8(uint32_t x, uint32_t y) {
+    const uint32_t t = (x | 0x80808080u) - ((y & 0x7f7f7f7fu) + 0x01010101u);
+    return (x & ~y) | (~(x ^ y) & t);
+}
+__device__ __forceinline__ uint32_t arc9(const uint32_t (&f)[16]) {
+    uint32_t t3[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) t3[k] = f[k] & f[(k + 1) & 15] & f[(k + 2) & 15];
+    uint32_t any = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) any |= t3[k] & t3[(k + 3) & 15] & t3[(k + 6) & 15];
+    return any;
+}
+}  // namespace d9
+
+__global__ void __launch_bounds__(256, 3) k_detect9(const __grid_constant__ ExtractArgs a) {
+    using namespace d9;
+    __shared__ uint32_t s_img[SH * SWW];
+    __shared__ int s_grad[GY * GX];  // (gx & 0xffff) | gy << 16
+    __shared__ float s_resp[NX * NY];
+    __shared__ short s_cand[NX * NY];
+    __shared__ int s_ncand;
+
+    const int ri = blockIdx.y;
+    const DevRegion rg = a.regions[ri];
+    const int t = blockIdx.x;
+    if (t >= rg.ntiles) return;
+    const DevImage im = a.images[rg.img];
+    const int ox = rg.x0 + (t % rg.tiles_x) * TX;
+    const int oy = rg.y0 + (t / rg.tiles_x) * TY;
+    const int fx0 = (ox - 1) & ~3;  // first FAST word (ox >= 3)
+    const int gx0 = fx0 - 4, gy0 = oy - 5;
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid == 0) s_ncand = 0;
+
+    // ---- stage: SH rows x SWW words
+    const bool inside = gx0 >= 0 && gy0 >= 0 && gx0 + SB <= im.w && gy0 + SH <= im.h && (im.w & 3) == 0 &&
+                        (reinterpret_cast<uintptr_t>(im.p) & 3) == 0;
+    if (inside) {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(im.p + static_cast<size_t>(gy0) * im.w + gx0);
+        const int pitch = im.w >> 2;
+        for (int i = tid; i < SH * SWW; i += 256) {
+            const int r = i / SWW, q = i - r * SWW;
+            s_img[i] = __ldg(src + static_cast<size_t>(r) * pitch + q);
+        }
+    } else {  // clamped bytes; clamped texels never reach a valid test
+        for (int i = tid; i < SH * SWW; i += 256) {
+            const int r = i / SWW, q = i - r * SWW;
+            const uint8_t* row = im.p + static_cast<size_t>(min(max(gy0 + r, 0), im.h - 1)) * im.w;
+            uint32_t v = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                v |= static_cast<uint32_t>(__ldg(row + min(max(gx0 + 4 * q + b, 0), im.w - 1))) << (8 * b);
+            s_img[i] = v;
+        }
+    }
+    for (int i = tid; i < NX * NY; i += 256) s_resp[i] = __int_as_float(0x7fc00000);
+    __syncthreads();
+
+    // ---- gradients (integer central differences) over the Harris support
+    {
+        const uint8_t* sb = reinterpret_cast<const uint8_t*>(s_img);
+        const int xo = ox - fx0;  // gradient column gc sits at staged byte gc + xo
+        for (int i = tid; i < GY * GX; i += 256) {
+            const int gr = i / GX, gc = i - gr * GX;
+            const uint8_t* p = sb + (gr + 1) * SB + gc + xo;
+            const int gx = int(p[1]) - int(p[-1]);
+            const int gy = int(p[SB]) - int(p[-SB]);
+            s_grad[i] = (gx & 0xffff) | (gy << 16);
+        }
+    }
+
+    // ---- FAST-9, four pixels per task (row r of the response grid, word j)
+    {
+        const uint32_t T4 = static_cast<uint32_t>(a.fast_t) * 0x01010101u;
+        const int cx_lo = max(rg.x0, ox - 1), cx_hi = min(rg.x1, ox + TX + 1);
+#pragma unroll 1
+        for (int t0 = 0; t0 < NTASK; t0 += 256) {
+            const int task = t0 + tid;
+            const bool valid = task < NTASK;
+            const int tk = valid ? task : 0;
+            const int r = tk / FW, j = tk - r * FW;
+            const uint32_t* w0 = s_img + (r + 1) * SWW + j;  // row y-3, word j-1 of the centre
+            uint32_t wv[7][3];
+#pragma unroll
+            for (int dy = 0; dy < 7; ++dy)
+#pragma unroll
+                for (int q = 0; q < 3; ++q) wv[dy][q] = w0[dy * SWW + q];
+            const uint32_t C = wv[3][1];
+            const uint32_t Hc = __vaddus4(C, T4), Lc = __vsubus4(C, T4);
+            uint32_t fb[16], fd[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const int dx = ring_dx(k), dy = ring_dy(k) + 3;
+                uint32_t v;
+                if (dx == 0)
+                    v = wv[dy][1];
+                else if (dx > 0)
+                    v = __byte_perm(wv[dy][1], wv[dy][2], dx | (dx + 1) << 4 | (dx + 2) << 8 | (dx + 3) << 12);
                 else
-                    dev_fail(a.status, LP_CAPACITY_OVERFLOW);
-                // first radix digit of k_topn: top 12 key bits (sign, exponent, 3 mantissa bits)
-                atomicAdd(&a.hist[static_cast<size_t>(ri) * kTopnHistBins + (key >> 52)], 1u);
+                    v = __byte_perm(wv[dy][0], wv[dy][1], (4 + dx) | (5 + dx) << 4 | (6 + dx) << 8 | (7 + dx) << 12);
+                fb[k] = gt_u8(v, Hc);
+                fd[k] = gt_u8(Lc, v);
+            }
+            uint32_t F = (arc9(fb) | arc9(fd)) & 0x80808080u;
+            // scan area (lorb.hpp:196-198) and the tile + ring
+            const int y = oy - 1 + r, x4 = fx0 + 4 * j;
+            if (!valid || y < rg.y0 || y >= rg.y1) F = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (x4 + b < cx_lo || x4 + b >= cx_hi) F &= ~(0x80u << (8 * b));
+            // harris_response's window test (lorb.hpp:232-234)
+            if (F && (x4 - 4 < 0 || x4 + 3 + 4 >= im.w || y - 4 < 0 || y + 4 >= im.h)) {
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int x = x4 + b;
+                    if ((F >> (8 * b + 7)) & 1u && (x - 4 < 0 || x + 4 >= im.w || y - 4 < 0 || y + 4 >= im.h)) {
+                        dev_fail(a.status, LP_WINDOW_OUT_OF_BOUNDS);
+                        F &= ~(0x80u << (8 * b));
+                    }
+                }
+            }
+            // warp prefix of the corner counts, one shared atomic per warp
+            const int n = __popc(F);
+            int incl = n;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += v;
+            }
+            int base = 0;
+            if (lane == 31) base = atomicAdd(&s_ncand, incl);
+            base = __shfl_sync(0xffffffffu, base, 31) + incl - n;
+            const int gi = r * NX + (x4 - (ox - 1));
+            while (F) {
+                const int b = (__ffs(F) - 8) >> 3;
+                F &= F - 1;
+                s_cand[base++] = static_cast<short>(gi + b);
             }
         }
+    }
+    __syncthreads();
+
+    // ---- FP64 Harris over the candidates (lorb.hpp:235-247), exact x4 scaled
+    const int nc = s_ncand;
+    const double alpha = static_cast<double>(a.alpha);
+    for (int jj = tid; jj < nc; jj += 256) {
+        const int i = s_cand[jj];
+        const int ly = i / NX, lx = i - ly * NX;
+        const int* g0 = s_grad + ly * GX + lx;  // tap (u, v) = (-3, -3)
+        double sa = 0.0, sb = 0.0, sc = 0.0;
+#pragma unroll
+        for (int v = 0; v < 7; ++v)
+#pragma unroll
+            for (int u = 0; u < 7; ++u) {
+                const int g = g0[v * GX + u];
+                const double ix = static_cast<double>(static_cast<short>(g & 0xffff));
+                const double iy = static_cast<double>(g >> 16);
+                const double wt = a.hw[v * 7 + u];
+                const double wx = dmul(wt, ix), wy = dmul(wt, iy);
+                sa = dadd(sa, dmul(wx, ix));
+                sb = dadd(sb, dmul(wy, iy));
+                sc = dadd(sc, dmul(wx, iy));
+            }
+        sa = dmul(sa, 0.25);
+        sb = dmul(sb, 0.25);
+        sc = dmul(sc, 0.25);
+        const double s = dadd(sa, sb);
+        const double r = dsub(dsub(dmul(sa, sb), dmul(sc, sc)), dmul(dmul(alpha, s), s));
+        const float rf = __double2float_rn(r);
+        if (rf >= a.threshold) s_resp[i] = rf;
+    }
+    __syncthreads();
+
+    // ---- 3x3 NMS over the tile's candidates; survivors -> key list
+    for (int b0 = 0; b0 < nc; b0 += 256) {
+        const int jj = b0 + tid;
+        bool keep = false;
+        uint64_t key = 0;
+        if (jj < nc) {
+            const int i = s_cand[jj];
+            const int ly = i / NX, lx = i - ly * NX;
+            const float r = s_resp[i];
+            if (lx >= 1 && lx <= TX && ly >= 1 && ly <= TY && r == r) {
+                keep = nms_wins(s_resp, i, r);
+                key = kp_key(r, ox + lx - 1, oy + ly - 1);
+            }
+        }
+        emit_survivor(a, ri, keep, key);
     }
 }
 
@@ -531,10 +748,10 @@ void extract_launch(const ExtractArgs& a, cudaStream_t s) {
     if (a.nregions == 0) return;
     LPB_CUDA(cudaMemsetAsync(a.surv_count, 0, sizeof(unsigned) * a.nregions, s));
     LPB_CUDA(cudaMemsetAsync(a.hist, 0, sizeof(unsigned) * kTopnHistBins * a.nregions, s));
-    if (a.total_tiles > 0) {
+    if (a.max_tiles > 0) {
         // the local name keeps the profiler key "k_detect/0" for either instance
-        auto* k_detect = (a.harris_r == 3 && a.fast_arc == 9) ? &lpb::k_detect<3, 9> : &lpb::k_detect<0, 0>;
-        LPB_LAUNCH(k_detect, a.total_tiles, 256, 0, s, a);
+        auto* k_detect = (a.harris_r == 3 && a.fast_arc == 9) ? &lpb::k_detect9 : &lpb::k_detect<0, 0>;
+        LPB_LAUNCH(k_detect, dim3(a.max_tiles, a.nregions), 256, 0, s, a);
     }
     if (a.top_n <= kTopnRankCap) {
         LPB_LAUNCH(k_topn, a.nregions, 1024, 0, s, a);

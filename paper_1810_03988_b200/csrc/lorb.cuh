@@ -10,11 +10,12 @@ struct DevRegion {
     int img;                 // index into the image table
     int x0, y0, x1, y1;      // scan area (non-empty)
     int rx0, ry0, rx1, ry1;  // the DetectionRegion itself (for the BRIEF crop)
-    int tiles_x, tile_base;
+    int tiles_x, ntiles;     // detect tiles (kDetTileX x kDetTileY) over the scan area
     int out_slot;            // which output group (camera) the keypoints belong to
 };
 
-constexpr int kDetTile = 32;     // output tile edge of the detect kernel
+constexpr int kDetTileX = 64;    // output tile of the detect kernel (columns)
+constexpr int kDetTileY = 32;    // (rows)
 constexpr int kMaxHarrisR = 6;   // harris_sigma <= 2 (radius ceil(3 sigma))
 constexpr int kMaxBlurR = 12;    // brief_blur_sigma <= 4
 constexpr int kTopnSortCap = 8192;
@@ -25,9 +26,10 @@ constexpr int kTopnHistBins = 4096;  // first radix digit: top 12 key bits
 struct ExtractArgs {
     const DevRegion* regions;
     int nregions;
-    int total_tiles;
+    int max_tiles;           // largest per-region tile count (grid.x; grid.y = region)
     const DevImage* images;
     const double* harris_w;  // (2R+1)^2
+    double hw[49];           // the same weights in the parameter bank when R <= 3
     int harris_r;
     float alpha, threshold;
     int fast_t, fast_arc;
