@@ -992,7 +992,7 @@ struct ComposeBuffers {
         ncams = ncams_;
         levels = levels_;
         bufs.clear();
-        win.assign(static_cast<size_t>(ncams) * levels, Win{0, 0, 0, 0});
+        win.assign(static_cast<size_t>(ncams) * levels, Win{0, 0, 0, 0, 0});
         args = ComposeArgs{};
         args.ncams = ncams;
         args.levels = levels;
@@ -1021,9 +1021,10 @@ struct ComposeBuffers {
                 const int y1 = std::min(args.H[k], (w0.y0 + w0.h + (1 << k) - 1) >> k);
                 w.w = std::max(0, x1 - w.x0);
                 w.h = std::max(0, y1 - w.y0);
+                w.p = (w.w + 3) & ~3;
                 win[c * levels + k] = w;
                 args.win[c][k] = w;
-                const size_t np = static_cast<size_t>(w.w) * w.h;
+                const size_t np = static_cast<size_t>(w.p) * w.h;
                 args.G[c][k] = static_cast<float*>(alloc(sizeof(float) * np));
                 args.M[c][k] = static_cast<float*>(alloc(sizeof(float) * np));
                 host_G[c * levels + k] = args.G[c][k];
@@ -1038,8 +1039,10 @@ struct ComposeBuffers {
                 total_rows += w.h;
             }
         }
-        for (int k = 1; k < levels; ++k)
-            args.R[k] = static_cast<float*>(alloc(sizeof(float) * static_cast<size_t>(args.W[k]) * args.H[k]));
+        for (int k = 1; k < levels; ++k) {
+            args.Rp[k] = (args.W[k] + 3) & ~3;
+            args.R[k] = static_cast<float*>(alloc(sizeof(float) * static_cast<size_t>(args.Rp[k]) * args.H[k]));
+        }
         if (analytic) {
             args.runs_overflow_base = static_cast<int>(total_rows * kRunSlots);
             args.runs_cap = static_cast<int>(std::min<size_t>(total_rows * (kRunSlots + 4) + 4096, 1u << 30));
@@ -1065,9 +1068,9 @@ static void check_levels(int w, int h, int levels) {  // gaussian_pyramid, imgop
     }
 }
 
-__global__ void k_deinterleave(const float* in, int np, int ch, int c, float* out) {
+__global__ void k_deinterleave(const float* in, int w, int np, int ch, int c, float* out, int pitch) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < np) out[i] = in[static_cast<size_t>(i) * ch + c];
+    if (i < np) out[(i / w) * pitch + i % w] = in[static_cast<size_t>(i) * ch + c];
 }
 __global__ void k_interleave_u8(const uint8_t* in, int np, int ch, int c, uint8_t* out) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1085,21 +1088,23 @@ extern "C" lp_status lp_multiband_blend(lp_ctx* ctx, const float* images, const 
         const size_t np = static_cast<size_t>(w) * h;
         In<float> di(images, np * ch * n, s), dm(masks, np * n, s);
         ComposeBuffers cb;
-        std::vector<Win> full(n, Win{0, 0, w, h});
+        std::vector<Win> full(n, Win{0, 0, w, h, 0});
         cb.build(n, levels, w, h, full, false, s);
+        const size_t pitch = cb.win[0].p;  // window rows are padded to float4
         DBuf o1(np, s);
         Out<uint8_t> dout(out, np * ch, s);
         cb.args.out = o1.as<uint8_t>();
         for (int c = 0; c < n; ++c)
-            LPB_CUDA(cudaMemcpyAsync(cb.host_M[c * levels], dm.d + np * c, sizeof(float) * np, cudaMemcpyDeviceToDevice, s));
+            LPB_CUDA(cudaMemcpy2DAsync(cb.host_M[c * levels], sizeof(float) * pitch, dm.d + np * c, sizeof(float) * w,
+                                       sizeof(float) * w, h, cudaMemcpyDeviceToDevice, s));
         for (int cc = 0; cc < ch; ++cc) {
             for (int c = 0; c < n; ++c) {
                 if (ch == 1)
-                    LPB_CUDA(cudaMemcpyAsync(cb.host_G[c * levels], di.d + np * c, sizeof(float) * np,
-                                             cudaMemcpyDeviceToDevice, s));
+                    LPB_CUDA(cudaMemcpy2DAsync(cb.host_G[c * levels], sizeof(float) * pitch, di.d + np * c,
+                                               sizeof(float) * w, sizeof(float) * w, h, cudaMemcpyDeviceToDevice, s));
                 else
-                    LPB_LAUNCH(k_deinterleave, cdiv(np, 256), 256, 0, s, di.d + np * ch * c, static_cast<int>(np), ch,
-                               cc, cb.host_G[c * levels]);
+                    LPB_LAUNCH(k_deinterleave, cdiv(np, 256), 256, 0, s, di.d + np * ch * c, w, static_cast<int>(np),
+                               ch, cc, cb.host_G[c * levels], static_cast<int>(pitch));
             }
             blend_launch(cb.args, s);
             if (ch == 1)

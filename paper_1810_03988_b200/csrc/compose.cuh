@@ -8,11 +8,13 @@ namespace lpb {
 // it is exactly zero in the reference's full-canvas arrays.
 struct Win {
     int x0, y0, w, h;
+    int p;  // row pitch in elements (w rounded up to a multiple of 4: float4 rows)
 };
 
 constexpr int kMaxCompCams = 16;   // cameras per rig on the fused compositor path
 constexpr int kMaxCompLevels = 12; // blend levels (canvas >= 2^11 px per side for 12)
 constexpr int kRunSlots = 4;       // coverage runs stored inline per window row
+constexpr int kBlendAlignX = 64;   // level-0 window x alignment (blend tile width at level 0)
 
 // Passed by value (constant bank): all per-camera geometry and pointers.
 struct ComposeArgs {
@@ -33,6 +35,7 @@ struct ComposeArgs {
     int runs_overflow_base;
     int* runs_used;                            // overflow allocations (rows with > kRunSlots runs)
     float* R[kMaxCompLevels];                  // collapse buffers, levels >= 1
+    int Rp[kMaxCompLevels];                    // their row pitch (W[k] rounded up to 4)
     float down_taps[7];                        // gaussian_kernel(1.0f)
     DevImage src[kMaxCompCams];                // u8 grayscale cameras
     double hinv[kMaxCompCams][9];
