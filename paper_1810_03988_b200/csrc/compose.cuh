@@ -43,6 +43,10 @@ struct ComposeArgs {
     int* status;
 };
 
+// k_pyr_down output tile (level k+1) and its staged level-k box
+constexpr int PD2_TX = 64, PD2_TY = 16;
+constexpr int PD2_BW = 2 * PD2_TX + 8, PD2_BH = 2 * PD2_TY + 6;  // box 136 x 38 (134 used; rows of 16 B)
+
 // Full per-frame compositor: warp, coverage runs, pyramids, band blend + collapse.
 void compose_launch(const ComposeArgs& a, cudaStream_t s);
 // Pyramid + blend + collapse only (level-0 images and masks already in G/M).
