@@ -477,10 +477,12 @@ def main():
         byts = lib.lp_rig_algorithmic_bytes(rig.rig, dom.encode())
         peak, peak_src = measured_peak_hbm()
         achieved = byts / (avg * 1e-3) / 1e9 if byts > 0 else None
+        # DRAM bytes of the same launch from the committed ncu --set full capture
+        # (scripts/ncu_traffic.py -> profiles/ncu_traffic.json), or null
         traffic = None
         try:
             nj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-            traffic = nj.get(args.config, {}).get(dom.split("/")[0] + "/" + dom.split("/")[1])
+            traffic = nj.get(args.config, {}).get(dom, {}).get("traffic_bytes")
         except Exception:
             pass
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,

@@ -237,10 +237,33 @@ typedef struct lp_frame_out {
     float stage_ms[4];        /* out: detect, describe, match_estimate, warp_blend (device time) */
 } lp_frame_out;
 
+/* RigLayout::Camera (pipeline.hpp:240-247): a rectifying pre-transform
+ * (identity = none) and an optional crop (DetectionRegion, camera_id unused). */
+typedef struct lp_camera {
+    lp_homography pre_transform;
+    int has_crop;
+    lp_region crop;
+} lp_camera;
+
+/* StitchEngine::stage_rectify_crop (pipeline.hpp:391-417) for one frame: per
+ * camera, warp_image(to_f32(img), pre_transform, own w x h canvas) +
+ * to_u8_image when pre_transform is not exactly the identity, then the crop.
+ * Errors: SingularHomography (|det| < 1e-9), BadParams (crop outside image).
+ * images / outputs host or device; outputs[c] receives out_w[c] x out_h[c]
+ * bytes (at most w * h). */
+lp_status lp_rectify_crop(lp_ctx* ctx, int ncams, int w, int h, const lp_camera* cams,
+                          const uint8_t* const* images, uint8_t* const* outputs, int* out_w, int* out_h);
+
 /* StitchEngine(RigLayout{ncams identity cameras, overlap}, StitchParams, K),
  * pipeline.hpp:343-350; all cameras w x h grayscale. */
 lp_status lp_rig_create(lp_ctx* ctx, int ncams, int w, int h, const lp_params* params,
                         lp_rig** out);
+/* The same engine over a RigLayout (pipeline.hpp:240-247): every w x h raw
+ * frame passes stage_rectify_crop on the device before detection. The
+ * rectified cameras must share one size (the device rig's frame geometry);
+ * lp_rig_panorama_capacity and the stages use that size. */
+lp_status lp_rig_create_layout(lp_ctx* ctx, int ncams, int w, int h, const lp_camera* cams,
+                               const lp_params* params, lp_rig** out);
 void lp_rig_destroy(lp_rig* rig);
 /* One frame through detect -> describe -> match_estimate (HomographyCache,
  * pipeline.hpp:259-286) -> warp_blend. images[c] host or device. */

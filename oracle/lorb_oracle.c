@@ -1533,3 +1533,52 @@ int orc_synth_rotate(const uint8_t* img, int w, int h, double degrees, uint8_t* 
         }
     return LP_OK;
 }
+
+/* StitchEngine::stage_rectify_crop, pipeline.hpp:391-417: per camera
+ * warp_image(to_f32(img), pre_transform, own canvas) + to_u8_image when the
+ * pre-transform is not exactly the identity (compose.hpp:72-95,
+ * image.hpp:80-85), then the crop (BadParams when outside the image). */
+int orc_rectify_crop(int ncams, int w, int h, const lp_camera* cams, const uint8_t* const* images,
+                     uint8_t* const* outputs, int* out_w, int* out_h) {
+    static const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    const size_t np = (size_t)w * h;
+    float* f32 = (float*)malloc(sizeof(float) * np);
+    float* warped = (float*)malloc(sizeof(float) * np);
+    float* cov = (float*)malloc(sizeof(float) * np);
+    uint8_t* tmp = (uint8_t*)malloc(np);
+    int st = LP_OK;
+    for (int c = 0; c < ncams && st == LP_OK; ++c) {
+        int identity = 1;
+        for (int j = 0; j < 9; ++j)
+            if (!(cams[c].pre_transform.h[j] == I[j])) identity = 0;
+        if (identity) {
+            memcpy(tmp, images[c], np);
+        } else {
+            const lp_canvas self = {w, h, 0, 0};
+            for (size_t i = 0; i < np; ++i) f32[i] = (float)images[c][i];
+            st = orc_warp_image(f32, w, h, 1, &cams[c].pre_transform, &self, warped, cov);
+            if (st) break;
+            for (size_t i = 0; i < np; ++i) tmp[i] = to_u8(warped[i]);
+        }
+        int x0 = 0, y0 = 0, cw = w, ch = h;
+        if (cams[c].has_crop) {
+            const lp_region r = cams[c].crop;
+            if (r.x0 < 0 || r.y0 < 0 || r.x1 > w || r.y1 > h || r.x1 - r.x0 < 1 || r.y1 - r.y0 < 1) {
+                st = fail(LP_BAD_PARAMS, "rectify_crop: crop outside image");
+                break;
+            }
+            x0 = r.x0;
+            y0 = r.y0;
+            cw = r.x1 - r.x0;
+            ch = r.y1 - r.y0;
+        }
+        for (int y = 0; y < ch; ++y) memcpy(outputs[c] + (size_t)y * cw, tmp + (size_t)(y + y0) * w + x0, cw);
+        out_w[c] = cw;
+        out_h[c] = ch;
+    }
+    free(f32);
+    free(warped);
+    free(cov);
+    free(tmp);
+    return st;
+}

@@ -55,6 +55,8 @@ int orc_synth_planted_pair(int w, int h, double overlap, uint64_t seed, uint8_t*
 int orc_synth_sequence_frame(int w, int h, double overlap, uint64_t seed, uint64_t frame,
                              uint8_t* left, uint8_t* right);
 int orc_synth_rotate(const uint8_t* img, int w, int h, double degrees, uint8_t* out);
+int orc_rectify_crop(int ncams, int w, int h, const lp_camera* cams, const uint8_t* const* images,
+                     uint8_t* const* outputs, int* out_w, int* out_h);
 int orc_stitch_frame(int ncams, int w, int h, const lp_params* params,
                      const uint8_t* const* images, uint64_t frame_index, lp_frame_out* out);
 

@@ -552,6 +552,89 @@ int ref_stitch_frame(int ncams, int w, int h, const lp_params* params,
     });
 }
 
+// ---- RigLayout with rectification / crops (pipeline.hpp:240-247, 391-417) ----
+static RigLayout rig_layout_cams(int ncams, double overlap, const lp_camera* cams) {
+    RigLayout layout = rig_layout(ncams, overlap);
+    for (int c = 0; c < ncams; ++c) {
+        for (int j = 0; j < 9; ++j) layout.cameras[c].pre_transform.h[j] = cams[c].pre_transform.h[j];
+        if (cams[c].has_crop) {
+            const lp_region& r = cams[c].crop;
+            layout.cameras[c].crop = DetectionRegion{r.x0, r.y0, r.x1, r.y1, c};
+        }
+    }
+    return layout;
+}
+
+// StitchEngine::stage_rectify_crop alone; outputs[c] >= w*h bytes
+int ref_rectify_crop(int ncams, int w, int h, const lp_camera* cams, const std::uint8_t* const* images,
+                     std::uint8_t* const* outputs, int* out_w, int* out_h) {
+    return guard([&] {
+        lp_params p;
+        ref_params_default(&p);
+        StitchEngine eng(rig_layout_cams(ncams, p.overlap_fraction, cams), stitch_params(&p), PipelineConfig{});
+        FramePacket pkt;
+        for (int c = 0; c < ncams; ++c) pkt.images.push_back(u8_image(images[c], w, h, 1));
+        eng.stage_rectify_crop(pkt);
+        for (int c = 0; c < ncams; ++c) {
+            out_w[c] = pkt.images[c].width;
+            out_h[c] = pkt.images[c].height;
+            std::memcpy(outputs[c], pkt.images[c].data.data(), pkt.images[c].data.size());
+        }
+    });
+}
+
+// one frame through the serial stage bodies over a RigLayout
+int ref_stitch_frame_layout(int ncams, int w, int h, const lp_camera* cams, const lp_params* params,
+                            const std::uint8_t* const* images, std::uint64_t frame_index, lp_frame_out* out) {
+    return guard([&] {
+        PipelineConfig pc;
+        pc.mode = PipelineMode::Serial;
+        pc.homography_refresh = params->homography_refresh;
+        StitchEngine eng(rig_layout_cams(ncams, params->overlap_fraction, cams), stitch_params(params), pc);
+        FramePacket pkt;
+        pkt.frame_index = frame_index;
+        for (int c = 0; c < ncams; ++c) pkt.images.push_back(u8_image(images[c], w, h, 1));
+        pkt.keypoints.resize(ncams);
+        pkt.descriptors.resize(ncams);
+        pkt.pair_matches.resize(ncams - 1);
+        eng.stage_rectify_crop(pkt);
+        eng.stage_detect(pkt);
+        eng.stage_describe(pkt);
+        eng.stage_match_estimate(pkt);
+        eng.stage_warp_blend(pkt);
+        const int W2 = 2 * words(params->extraction.n_d);
+        std::vector<std::pair<int, int>> dims;
+        for (int c = 0; c < ncams; ++c) {
+            dims.emplace_back(pkt.images[c].width, pkt.images[c].height);
+            if (out->kp_counts) out->kp_counts[c] = static_cast<int>(pkt.keypoints[c].size());
+            for (std::size_t i = 0; i < pkt.keypoints[c].size() && static_cast<int>(i) < out->cap_kp; ++i) {
+                if (out->keypoints) out->keypoints[static_cast<std::size_t>(c) * out->cap_kp + i] = to_lp(pkt.keypoints[c][i]);
+                if (out->descriptors)
+                    pack_desc(pkt.descriptors[c][i],
+                              out->descriptors + (static_cast<std::size_t>(c) * out->cap_kp + i) * W2);
+            }
+            if (out->homographies)
+                for (int j = 0; j < 9; ++j) out->homographies[c].h[j] = pkt.homographies[c].h[j];
+        }
+        for (int p = 0; p + 1 < ncams; ++p) {
+            if (out->match_counts) out->match_counts[p] = static_cast<int>(pkt.pair_matches[p].size());
+            for (std::size_t i = 0; i < pkt.pair_matches[p].size() && static_cast<int>(i) < out->cap_matches; ++i)
+                if (out->matches) {
+                    const Match& m = pkt.pair_matches[p][i];
+                    out->matches[static_cast<std::size_t>(p) * out->cap_matches + i] =
+                        lp_match{m.query_id, m.train_id, m.distance, m.quality};
+                }
+        }
+        Canvas cv = compute_canvas(dims, pkt.homographies);
+        out->canvas = lp_canvas{cv.width, cv.height, cv.origin_x, cv.origin_y};
+        out->estimated = 1;
+        if (out->panorama) {
+            if (pkt.composite.data.size() > out->pano_cap) throw CapacityOverflow("panorama capacity");
+            std::memcpy(out->panorama, pkt.composite.data.data(), pkt.composite.data.size());
+        }
+    });
+}
+
 // CPU baseline: runs StitchEngine::run over `nframes` copies of the given
 // frame (pipeline.hpp:369-387). mode 0 = serial, 1 = pipelined. Reports the
 // reference's own Metrics (frames_out / wall_seconds, per-stage means in ms,

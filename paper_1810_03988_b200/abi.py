@@ -62,6 +62,11 @@ class Homography(C.Structure):
     _fields_ = [("h", C.c_double * 9)]
 
 
+class Camera(C.Structure):
+    """RigLayout::Camera (pipeline.hpp:240-247): pre_transform + optional crop."""
+    _fields_ = [("pre_transform", Homography), ("has_crop", C.c_int), ("crop", Region)]
+
+
 class Canvas(C.Structure):
     _fields_ = [("width", C.c_int), ("height", C.c_int), ("origin_x", C.c_int),
                 ("origin_y", C.c_int)]
@@ -103,6 +108,7 @@ P = C.c_void_p  # generic pointer (host numpy data or device address)
 
 # name -> argtypes after the (optional) context argument
 _PROTOS = {
+    "rectify_crop": [C.c_int, C.c_int, C.c_int, P, P, P, c_intp, c_intp],
     "fast_corners": [P, C.c_int, C.c_int, C.c_int, Region, C.c_int, C.c_int, P, C.c_int, c_intp],
     "harris_response": [P, C.c_int, C.c_int, C.c_int, P, C.c_int, C.c_float, C.c_float, P],
     "nms": [P, C.c_int, C.c_int, P, c_intp],
@@ -145,6 +151,8 @@ _ORACLE_EXTRA = {
 }
 
 _REF_ONLY = {
+    "stitch_frame_layout": [C.c_int, C.c_int, C.c_int, P, C.POINTER(Params), P, C.c_uint64,
+                            C.POINTER(FrameOut)],
     "lsh_query": [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, P, C.c_int, C.c_int, P,
                   C.c_int, c_intp],
     "run_engine": [C.c_int, C.c_int, C.c_int, C.POINTER(Params), P, C.c_int, C.c_int, C.c_int,

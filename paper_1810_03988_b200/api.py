@@ -320,7 +320,33 @@ class AbiWrapper:
         return out
 
     # ---- whole frame ----
-    def stitch_frame(self, images, params, frame_index=0, pano_cap=None):
+    @staticmethod
+    def cameras(specs):
+        """[(pre_transform 3x3 or None, crop (x0, y0, x1, y1) or None), ...] -> Camera array."""
+        arr = (abi.Camera * len(specs))()
+        for c, (hom, crop) in enumerate(specs):
+            h = np.eye(3) if hom is None else np.asarray(hom, np.float64).reshape(3, 3)
+            arr[c].pre_transform.h[:] = list(h.ravel())
+            arr[c].has_crop = 0 if crop is None else 1
+            if crop is not None:
+                arr[c].crop = abi.Region(*[int(v) for v in crop], c)
+        return arr
+
+    def rectify_crop(self, images, specs):
+        """stage_rectify_crop (pipeline.hpp:391-417): list of u8 images."""
+        ncams = len(images)
+        h, w = images[0].shape
+        imgs = [np.ascontiguousarray(i, np.uint8) for i in images]
+        outs = [np.zeros(w * h, np.uint8) for _ in images]
+        ow = np.zeros(ncams, np.int32)
+        oh = np.zeros(ncams, np.int32)
+        self._call("rectify_crop", ncams, w, h, self.cameras(specs),
+                   (C.c_void_p * ncams)(*[i.ctypes.data for i in imgs]),
+                   (C.c_void_p * ncams)(*[o.ctypes.data for o in outs]),
+                   ow.ctypes.data_as(abi.c_intp), oh.ctypes.data_as(abi.c_intp))
+        return [outs[c][:ow[c] * oh[c]].reshape(oh[c], ow[c]).copy() for c in range(ncams)]
+
+    def stitch_frame(self, images, params, frame_index=0, pano_cap=None, cameras=None):
         ncams = len(images)
         h, w = images[0].shape
         imgs = [np.ascontiguousarray(i, np.uint8) for i in images]
@@ -347,7 +373,11 @@ class AbiWrapper:
         fo.match_counts = mc.ctypes.data_as(abi.c_intp)
         fo.matches = mt.ctypes.data_as(C.POINTER(abi.Match))
         fo.cap_matches = cap_m
-        self._call("stitch_frame", ncams, w, h, C.byref(params), ptrs, frame_index, C.byref(fo))
+        if cameras is None:
+            self._call("stitch_frame", ncams, w, h, C.byref(params), ptrs, frame_index, C.byref(fo))
+        else:  # RigLayout (reference only)
+            self._call("stitch_frame_layout", ncams, w, h, self.cameras(cameras), C.byref(params), ptrs,
+                       frame_index, C.byref(fo))
         cv = fo.canvas
         return dict(
             canvas=(cv.width, cv.height, cv.origin_x, cv.origin_y),

@@ -1118,4 +1118,71 @@ extern "C" lp_status lp_multiband_blend(lp_ctx* ctx, const float* images, const 
     });
 }
 
+namespace lpb {
+// RigLayout cameras -> device RectCam descriptors (no pointers yet), in
+// stage_rectify_crop's order of checks (pipeline.hpp:393-414)
+static std::vector<RectCam> rect_cams(int ncams, int w, int h, const lp_camera* cams) {
+    std::vector<RectCam> out(ncams);
+    for (int c = 0; c < ncams; ++c) {
+        const lp_camera& cam = cams[c];
+        RectCam& rc = out[c];
+        rc.src = nullptr;
+        rc.dst = nullptr;
+        static const double I[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+        rc.identity = 1;
+        for (int j = 0; j < 9; ++j)
+            if (!(cam.pre_transform.h[j] == I[j])) rc.identity = 0;
+        if (!rc.identity) {
+            if (std::abs(host::h_det(cam.pre_transform.h)) < 1e-9)
+                throw Status(LP_SINGULAR_HOMOGRAPHY, "warp_image: singular homography");
+            host::h_inverse(cam.pre_transform.h, rc.hinv);
+        } else {
+            for (int j = 0; j < 9; ++j) rc.hinv[j] = I[j];
+        }
+        rc.x0 = 0;
+        rc.y0 = 0;
+        rc.w = w;
+        rc.h = h;
+        if (cam.has_crop) {
+            const lp_region& r = cam.crop;
+            if (r.x0 < 0 || r.y0 < 0 || r.x1 > w || r.y1 > h || r.x1 - r.x0 < 1 || r.y1 - r.y0 < 1)
+                throw Status(LP_BAD_PARAMS, "rectify_crop: crop outside image");
+            rc.x0 = r.x0;
+            rc.y0 = r.y0;
+            rc.w = r.x1 - r.x0;
+            rc.h = r.y1 - r.y0;
+        }
+    }
+    return out;
+}
+}  // namespace lpb
+
+extern "C" lp_status lp_rectify_crop(lp_ctx* ctx, int ncams, int w, int h, const lp_camera* cams,
+                                     const uint8_t* const* images, uint8_t* const* outputs, int* out_w,
+                                     int* out_h) {
+    return guard([&] {
+        if (ncams < 1 || ncams > kMaxCams || w < 1 || h < 1) throw Status(LP_BAD_PARAMS, "rectify_crop: bad dims");
+        cudaStream_t s = ctx->stream;
+        auto rc = rect_cams(ncams, w, h, cams);
+        const size_t fb = static_cast<size_t>(w) * h;
+        std::vector<std::unique_ptr<In<uint8_t>>> ins;
+        std::vector<std::unique_ptr<Out<uint8_t>>> outs;
+        int mw = 0, mh = 0;
+        for (int c = 0; c < ncams; ++c) {
+            ins.push_back(std::make_unique<In<uint8_t>>(images[c], fb, s));
+            outs.push_back(std::make_unique<Out<uint8_t>>(outputs[c], static_cast<size_t>(rc[c].w) * rc[c].h, s));
+            rc[c].src = ins.back()->d;
+            rc[c].dst = outs.back()->d;
+            mw = std::max(mw, rc[c].w);
+            mh = std::max(mh, rc[c].h);
+            out_w[c] = rc[c].w;
+            out_h[c] = rc[c].h;
+        }
+        DBuf drc = upload(rc, s);
+        rectify_launch(drc.as<RectCam>(), ncams, w, h, mw, mh, s);
+        for (int c = 0; c < ncams; ++c) outs[c]->finish(s, static_cast<size_t>(rc[c].w) * rc[c].h);
+        LPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 #include "rig.inc"

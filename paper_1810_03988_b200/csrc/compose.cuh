@@ -47,6 +47,17 @@ struct ComposeArgs {
 constexpr int PD2_TX = 64, PD2_TY = 16;
 constexpr int PD2_BW = 2 * PD2_TX + 8, PD2_BH = 2 * PD2_TY + 6;  // box 136 x 38 (134 used; rows of 16 B)
 
+// stage_rectify_crop (pipeline.hpp:391-417) of one camera: dst (w x h, the
+// crop's size) from src (in_w x in_h)
+struct RectCam {
+    const uint8_t* src;
+    uint8_t* dst;
+    double hinv[9];  // inverse of pre_transform (Homography::inverse)
+    int identity;    // pre_transform exactly the identity: crop copy only
+    int x0, y0, w, h;  // crop (the whole image when there is none)
+};
+void rectify_launch(const RectCam* cams, int ncams, int in_w, int in_h, int max_w, int max_h, cudaStream_t s);
+
 // Full per-frame compositor: warp, coverage runs, pyramids, band blend + collapse.
 void compose_launch(const ComposeArgs& a, cudaStream_t s);
 // Pyramid + blend + collapse only (level-0 images and masks already in G/M).

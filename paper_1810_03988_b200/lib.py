@@ -52,6 +52,9 @@ def load():
         lib.lp_params_default.restype = None
         lib.lp_rig_create.argtypes = [P, C.c_int, C.c_int, C.c_int, C.POINTER(abi.Params), C.POINTER(P)]
         lib.lp_rig_create.restype = C.c_int
+        lib.lp_rig_create_layout.argtypes = [P, C.c_int, C.c_int, C.c_int, P, C.POINTER(abi.Params),
+                                             C.POINTER(P)]
+        lib.lp_rig_create_layout.restype = C.c_int
         lib.lp_rig_destroy.argtypes = [P]
         lib.lp_rig_destroy.restype = None
         lib.lp_rig_stitch.argtypes = [P, P, C.c_uint64, C.POINTER(abi.FrameOut)]
@@ -122,10 +125,11 @@ class Lorb(AbiWrapper):
         self.lib.lp_params_default(C.byref(p))
         return p
 
-    def stitch_frame(self, images, params, frame_index=0, pano_cap=None):
-        """One frame through a fresh engine (the oracles' stitch_frame)."""
+    def stitch_frame(self, images, params, frame_index=0, pano_cap=None, cameras=None):
+        """One frame through a fresh engine (the oracles' stitch_frame);
+        `cameras` = RigLayout specs as for rectify_crop."""
         h, w = images[0].shape[:2]
-        rig = Rig(self, len(images), w, h, params)
+        rig = Rig(self, len(images), w, h, params, cameras=cameras)
         try:
             return rig.stitch(images, frame_index, pano_cap=pano_cap, details=True)
         finally:
@@ -135,13 +139,18 @@ class Lorb(AbiWrapper):
 class Rig:
     """StitchEngine for a chain of identical cameras (pipeline.hpp:341-721) on one GPU."""
 
-    def __init__(self, lorb, ncams, w, h, params):
+    def __init__(self, lorb, ncams, w, h, params, cameras=None):
         self.lorb = lorb
         self.lib = lorb.lib
         self.ncams, self.w, self.h = ncams, w, h
         self.params = params
         r = C.c_void_p()
-        _check(self.lib, self.lib.lp_rig_create(lorb.ctx, ncams, w, h, C.byref(params), C.byref(r)))
+        if cameras is None:
+            _check(self.lib, self.lib.lp_rig_create(lorb.ctx, ncams, w, h, C.byref(params), C.byref(r)))
+        else:  # RigLayout: stage_rectify_crop on ingest
+            cams = AbiWrapper.cameras(cameras)
+            _check(self.lib, self.lib.lp_rig_create_layout(lorb.ctx, ncams, w, h, cams, C.byref(params),
+                                                           C.byref(r)))
         self.rig = r
 
     def close(self):
