@@ -254,6 +254,22 @@ typedef struct lp_camera {
 lp_status lp_rectify_crop(lp_ctx* ctx, int ncams, int w, int h, const lp_camera* cams,
                           const uint8_t* const* images, uint8_t* const* outputs, int* out_w, int* out_h);
 
+/* brief_pattern (lorb.hpp:303-330): the n_d test pairs the engine draws from
+ * mt19937_64(seed) (StitchEngine ctor, pipeline.hpp:345). Host only. */
+lp_status lp_brief_pattern(int n_d, int patch_half, uint64_t seed, lp_pair* out);
+
+/* ---- frame ingest / egress formats ---- */
+/* load_pnm (image.hpp:88-126, binary P5/P6, maxval 255): with out == NULL or
+ * cap too small only the header is read into w/h/channels (returns
+ * CapacityOverflow when out is non-NULL and too small). Errors as the
+ * reference: FileNotFound, UnsupportedFormat, CorruptData. Host only. */
+lp_status lp_load_pnm(const char* path, uint8_t* out, size_t cap, int* w, int* h, int* channels);
+/* save_pnm (image.hpp:194-204): P5 for 1 channel, P6 for 3. Host only. */
+lp_status lp_save_pnm(const char* path, const uint8_t* data, int w, int h, int channels);
+/* The CLI sink's gray -> RGB triplication (cli.hpp:138-145) on the device:
+ * rgb[3i + c] = gray[i]; gray / rgb host or device. */
+lp_status lp_gray_to_rgb(lp_ctx* ctx, const uint8_t* gray, size_t n, uint8_t* rgb);
+
 /* StitchEngine(RigLayout{ncams identity cameras, overlap}, StitchParams, K),
  * pipeline.hpp:343-350; all cameras w x h grayscale. */
 lp_status lp_rig_create(lp_ctx* ctx, int ncams, int w, int h, const lp_params* params,
@@ -291,6 +307,10 @@ lp_status lp_rig_submit(lp_rig* rig, const uint8_t* const* images, uint64_t fram
                         uint8_t* panorama, size_t pano_cap, uint64_t* ticket);
 lp_status lp_rig_wait(lp_rig* rig, uint64_t ticket, lp_canvas* canvas);
 
+/* Egress format of lp_rig_submit / lp_rig_stitch panoramas: 1 = the PPM sink's
+ * 3-channel RGB (gray triplicated on the device before the copy out,
+ * cli.hpp:138-145; 3 x canvas bytes), 0 = gray (default). */
+lp_status lp_rig_set_egress(lp_rig* rig, int channels_rgb);
 /* Upper bound on panorama bytes for this rig's current homographies. */
 size_t lp_rig_panorama_capacity(lp_rig* rig);
 /* The stream the rig's work is enqueued on (cudaStream_t). */

@@ -11,7 +11,9 @@
 #include <cub/cub.cuh>
 
 #include <atomic>
+#include <cctype>
 #include <deque>
+#include <fstream>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -1181,6 +1183,104 @@ extern "C" lp_status lp_rectify_crop(lp_ctx* ctx, int ncams, int w, int h, const
         DBuf drc = upload(rc, s);
         rectify_launch(drc.as<RectCam>(), ncams, w, h, mw, mh, s);
         for (int c = 0; c < ncams; ++c) outs[c]->finish(s, static_cast<size_t>(rc[c].w) * rc[c].h);
+        LPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Frame ingest / egress formats
+namespace lpb {
+// pnm_read_token (image.hpp:88-103): skips whitespace and '#' comments
+static int pnm_token(std::istream& in) {
+    while (in) {
+        const int c = in.peek();
+        if (c == '#') {
+            while (in && in.get() != '\n') {
+            }
+        } else if (std::isspace(c)) {
+            in.get();
+        } else {
+            break;
+        }
+    }
+    int v = -1;
+    in >> v;
+    return v;
+}
+
+__global__ void k_gray_to_rgb(const uint8_t* __restrict__ g, size_t n, uint8_t* __restrict__ rgb) {
+    // 4 gray pixels -> 12 RGB bytes (three 32-bit words) per thread when aligned
+    const size_t i4 = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    if (i4 >= n) return;
+    if (i4 + 4 <= n && (reinterpret_cast<uintptr_t>(g + i4) & 3) == 0 && (reinterpret_cast<uintptr_t>(rgb + 3 * i4) & 3) == 0) {
+        const uint32_t v = *reinterpret_cast<const uint32_t*>(g + i4);
+        uint32_t* o = reinterpret_cast<uint32_t*>(rgb + 3 * i4);
+        o[0] = __byte_perm(v, 0, 0x1000);  // a a a b
+        o[1] = __byte_perm(v, 0, 0x2211);  // b b c c
+        o[2] = __byte_perm(v, 0, 0x3332);  // c d d d
+    } else {
+        for (size_t i = i4; i < n && i < i4 + 4; ++i) rgb[3 * i] = rgb[3 * i + 1] = rgb[3 * i + 2] = g[i];
+    }
+}
+void gray_to_rgb_launch(const uint8_t* g, size_t n, uint8_t* rgb, cudaStream_t s) {
+    if (n == 0) return;
+    LPB_LAUNCH(k_gray_to_rgb, cdiv(static_cast<long long>((n + 3) / 4), 256), 256, 0, s, g, n, rgb);
+}
+}  // namespace lpb
+
+extern "C" lp_status lp_brief_pattern(int n_d, int patch_half, uint64_t seed, lp_pair* out) {
+    return guard([&] {
+        if (n_d < 1 || patch_half < 1) throw Status(LP_BAD_PARAMS, "brief_pattern: bad parameters");
+        const auto pat = host::brief_pattern(n_d, patch_half, seed);
+        std::memcpy(out, pat.data(), sizeof(lp_pair) * pat.size());
+    });
+}
+
+extern "C" lp_status lp_load_pnm(const char* path, uint8_t* out, size_t cap, int* w, int* h, int* channels) {
+    return guard([&] {
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw Status(LP_FILE_NOT_FOUND, std::string(path));
+        char p = 0, n = 0;
+        in.get(p);
+        in.get(n);
+        if (p != 'P' || (n != '5' && n != '6'))
+            throw Status(LP_UNSUPPORTED_FORMAT, std::string(path) + ": not a binary PGM/PPM");
+        const int ch = n == '5' ? 1 : 3;
+        const int W = pnm_token(in), H = pnm_token(in), maxval = pnm_token(in);
+        if (!in || W < 1 || H < 1) throw Status(LP_CORRUPT_DATA, std::string(path) + ": bad header");
+        if (maxval != 255) throw Status(LP_UNSUPPORTED_FORMAT, std::string(path) + ": only maxval 255 supported");
+        in.get();  // single whitespace after maxval
+        *w = W;
+        *h = H;
+        *channels = ch;
+        const size_t bytes = static_cast<size_t>(W) * H * ch;
+        if (!out) return;
+        if (cap < bytes) throw Status(LP_CAPACITY_OVERFLOW, std::string(path) + ": output buffer too small");
+        in.read(reinterpret_cast<char*>(out), static_cast<std::streamsize>(bytes));
+        if (static_cast<size_t>(in.gcount()) != bytes)
+            throw Status(LP_CORRUPT_DATA, std::string(path) + ": truncated pixel data");
+    });
+}
+
+extern "C" lp_status lp_save_pnm(const char* path, const uint8_t* data, int w, int h, int channels) {
+    return guard([&] {
+        if (channels != 1 && channels != 3)
+            throw Status(LP_UNSUPPORTED_FORMAT, std::string(path) + ": only 1- or 3-channel images");
+        std::ofstream out(path, std::ios::binary);
+        if (!out) throw Status(LP_FILE_NOT_FOUND, std::string(path) + ": cannot open for writing");
+        out << (channels == 1 ? "P5\n" : "P6\n") << w << ' ' << h << "\n255\n";
+        out.write(reinterpret_cast<const char*>(data), static_cast<std::streamsize>(static_cast<size_t>(w) * h * channels));
+        if (!out) throw Status(LP_CORRUPT_DATA, std::string(path) + ": write failed");
+    });
+}
+
+extern "C" lp_status lp_gray_to_rgb(lp_ctx* ctx, const uint8_t* gray, size_t n, uint8_t* rgb) {
+    return guard([&] {
+        cudaStream_t s = ctx->stream;
+        In<uint8_t> g(gray, n, s);
+        Out<uint8_t> o(rgb, 3 * n, s);
+        gray_to_rgb_launch(g.d, n, o.d, s);
+        o.finish(s, 3 * n);
         LPB_CUDA(cudaStreamSynchronize(s));
     });
 }

@@ -55,6 +55,17 @@ def load():
         lib.lp_rig_create_layout.argtypes = [P, C.c_int, C.c_int, C.c_int, P, C.POINTER(abi.Params),
                                              C.POINTER(P)]
         lib.lp_rig_create_layout.restype = C.c_int
+        lib.lp_brief_pattern.argtypes = [C.c_int, C.c_int, C.c_uint64, P]
+        lib.lp_brief_pattern.restype = C.c_int
+        lib.lp_load_pnm.argtypes = [C.c_char_p, P, C.c_size_t, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                    C.POINTER(C.c_int)]
+        lib.lp_load_pnm.restype = C.c_int
+        lib.lp_save_pnm.argtypes = [C.c_char_p, P, C.c_int, C.c_int, C.c_int]
+        lib.lp_save_pnm.restype = C.c_int
+        lib.lp_gray_to_rgb.argtypes = [P, P, C.c_size_t, P]
+        lib.lp_gray_to_rgb.restype = C.c_int
+        lib.lp_rig_set_egress.argtypes = [P, C.c_int]
+        lib.lp_rig_set_egress.restype = C.c_int
         lib.lp_rig_destroy.argtypes = [P]
         lib.lp_rig_destroy.restype = None
         lib.lp_rig_stitch.argtypes = [P, P, C.c_uint64, C.POINTER(abi.FrameOut)]
@@ -125,6 +136,19 @@ class Lorb(AbiWrapper):
         self.lib.lp_params_default(C.byref(p))
         return p
 
+    def brief_pattern(self, n_d=256, patch_half=15, seed=42):
+        """brief_pattern (lorb.hpp:303-330), host side of the product library."""
+        out = np.zeros((n_d, 4), np.int32)
+        _check(self.lib, self.lib.lp_brief_pattern(n_d, patch_half, seed, out.ctypes.data))
+        return out
+
+    def gray_to_rgb(self, gray):
+        """The PPM sink's triplication (cli.hpp:138-145) on the device."""
+        g = np.ascontiguousarray(gray, np.uint8)
+        out = np.empty(g.shape + (3,), np.uint8)
+        _check(self.lib, self.lib.lp_gray_to_rgb(self.ctx, g.ctypes.data, g.size, out.ctypes.data))
+        return out
+
     def stitch_frame(self, images, params, frame_index=0, pano_cap=None, cameras=None):
         """One frame through a fresh engine (the oracles' stitch_frame);
         `cameras` = RigLayout specs as for rectify_crop."""
@@ -163,6 +187,10 @@ class Rig:
             self.close()
         except Exception:
             pass
+
+    def set_egress_rgb(self, on=True):
+        """Panoramas leave the device as 3-channel RGB (the PPM sink's format)."""
+        _check(self.lib, self.lib.lp_rig_set_egress(self.rig, 1 if on else 0))
 
     @property
     def stream(self):
@@ -238,3 +266,23 @@ class Rig:
                 matches=[mt[q, :mc[q]].copy() for q in range(ncams - 1)],
             )
         return out
+
+
+def load_pnm(path):
+    """load_pnm (image.hpp:88-126) through the C-ABI: (h, w) or (h, w, 3) uint8."""
+    lib = load()
+    w, h, ch = C.c_int(), C.c_int(), C.c_int()
+    p = os.fsencode(path)
+    _check(lib, lib.lp_load_pnm(p, None, 0, C.byref(w), C.byref(h), C.byref(ch)))
+    shape = (h.value, w.value) if ch.value == 1 else (h.value, w.value, 3)
+    out = np.empty(shape, np.uint8)
+    _check(lib, lib.lp_load_pnm(p, out.ctypes.data, out.size, C.byref(w), C.byref(h), C.byref(ch)))
+    return out
+
+
+def save_pnm(path, img):
+    """save_pnm (image.hpp:194-204): P5 for (h, w), P6 for (h, w, 3)."""
+    lib = load()
+    a = np.ascontiguousarray(img, np.uint8)
+    ch = 1 if a.ndim == 2 else a.shape[2]
+    _check(lib, lib.lp_save_pnm(os.fsencode(path), a.ctypes.data, a.shape[1], a.shape[0], ch))

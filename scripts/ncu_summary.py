@@ -39,7 +39,7 @@ def main(path):
             if m.startswith("dram__bytes"):
                 v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
             if m == "gpu__time_duration.sum":
-                v *= {"nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(u, 1)
+                v *= {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3, "ns": 1e-3, "us": 1, "ms": 1e3}.get(u, 1)
             out.append(f"{v * scale:10.2f}")
         print(r[ix["Kernel Name"]].split("(")[0][-34:].ljust(34) + " ".join(out))
 
