@@ -235,15 +235,17 @@ struct ExtractTables {
     int harris_r = 0, blur_r = 0;
     // the weights again in the kernel's parameter bank (k_detect9 reads them
     // as constant operands)
+    std::vector<float> tp;
     void fill(ExtractArgs& a) const {
         a.harris_w = harris_w.as<double>();
         a.harris_r = harris_r;
         for (size_t i = 0; i < 49; ++i) a.hw[i] = i < hw.size() ? hw[i] : 0.0;
+        for (size_t i = 0; i < 2 * kMaxBlurR + 1; ++i) a.btaps[i] = i < tp.size() ? tp[i] : 0.0f;
     }
     ExtractTables(const lp_extraction_config& c, const std::vector<lp_pair>& pat, cudaStream_t s) {
         hw = host::harris_weights(c.harris_sigma, &harris_r);
         if (harris_r > kMaxHarrisR) throw Status(LP_BAD_PARAMS, "harris_sigma too large for the device tile");
-        auto tp = host::gaussian_kernel(c.brief_blur_sigma);
+        tp = host::gaussian_kernel(c.brief_blur_sigma);
         blur_r = static_cast<int>(tp.size() / 2);
         if (blur_r > kMaxBlurR) throw Status(LP_BAD_PARAMS, "brief_blur_sigma too large");
         harris_w = upload(hw, s);

@@ -744,6 +744,115 @@ __global__ void __launch_bounds__(256) k_describe(ExtractArgs a, int warp_bytes)
     if (lane == 0) a.kp_out[static_cast<size_t>(rg.out_slot) * a.cap_slot + idx] = kp;
 }
 
+// ---------------------------------------------------------------------------
+// k_describe6: the default blur radius (sigma = 2 -> 13 taps), one warp per
+// keypoint. The 43x43 u8 patch is staged with 8 loads in flight per lane, the
+// horizontal pass is unrolled with the taps in the parameter bank, and the
+// vertical pass is evaluated only at the pattern's sample points, straight
+// into the tests: S(p) is the same 13-tap sum in the same order as the full
+// crop blur (imgops.hpp:50-72), so the descriptor is bit-identical while 512
+// instead of 961 vertical sums are formed and no 31x31 plane is stored
+// (7 KB of shared memory per warp instead of 11 KB).
+constexpr int D6_RB = 6;
+__global__ void __launch_bounds__(256) k_describe6(const __grid_constant__ ExtractArgs a, int warp_bytes) {
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    lp_pair* s_pairs = reinterpret_cast<lp_pair*>(s_dyn);
+    const int warps = blockDim.x / 32;
+    unsigned char* s_warp_base = s_dyn + ((a.n_d * sizeof(lp_pair) + 15) & ~15);
+    for (int i = threadIdx.x; i < a.n_d; i += blockDim.x) s_pairs[i] = a.pairs[i];
+    if (blockIdx.x == 0 && threadIdx.x < a.nslots) {
+        int tot = 0;
+        for (int r = 0; r < a.nregions; ++r)
+            if (a.regions[r].out_slot == static_cast<int>(threadIdx.x)) tot += a.count_region[r];
+        a.slot_count[threadIdx.x] = tot;
+    }
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gslot = blockIdx.x * warps + warp;
+    const int ri = gslot / a.top_n, i = gslot - ri * a.top_n;
+    if (ri >= a.nregions || i >= a.count_region[ri]) return;
+    const DevRegion rg = a.regions[ri];
+    const DevImage im = a.images[rg.img];
+    const lp_keypoint kp = a.kp_region[static_cast<size_t>(ri) * a.top_n + i];
+    int off = 0;
+    for (int r = 0; r < ri; ++r)
+        if (a.regions[r].out_slot == rg.out_slot) off += a.count_region[r];
+    const int idx = off + i;
+    const int P = a.patch_half;
+    const int pw = 2 * P + 1, iw = pw + 2 * D6_RB;
+
+    // smoothed_crop bounds (lorb.hpp:371-375) for the PatchOutOfBounds test (336-338)
+    const int margin = P + D6_RB;
+    const int cx0 = max(0, rg.rx0 - margin), cy0 = max(0, rg.ry0 - margin);
+    const int cx1 = min(im.w, rg.rx1 + margin), cy1 = min(im.h, rg.ry1 + margin);
+    if (kp.x - P < cx0 || kp.x + P >= cx1 || kp.y - P < cy0 || kp.y + P >= cy1) {
+        if (lane == 0) dev_fail(a.status, LP_PATCH_OUT_OF_BOUNDS);
+        return;
+    }
+    uint8_t* s_in = s_warp_base + static_cast<size_t>(warp) * warp_bytes;            // iw x iw u8
+    float* s_tmp = reinterpret_cast<float*>(s_in + ((iw * iw + 15) & ~15));          // iw x pw
+    const int bx = kp.x - P - D6_RB, by = kp.y - P - D6_RB;
+    // stage the u8 patch; 8 loads in flight per lane
+    for (int j0 = lane; j0 < iw * iw; j0 += 32 * 8) {
+        uint8_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = j0 + 32 * u;
+            v[u] = 0;
+            if (j < iw * iw) {
+                const int ly = j / iw, lx = j - ly * iw;
+                const int gx = min(max(bx + lx, 0), im.w - 1), gy = min(max(by + ly, 0), im.h - 1);
+                v[u] = __ldg(im.p + static_cast<size_t>(gy) * im.w + gx);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (j0 + 32 * u < iw * iw) s_in[j0 + 32 * u] = v[u];
+    }
+    __syncwarp();
+    // horizontal pass: every staged row, the pw patch columns
+    for (int j = lane; j < iw * pw; j += 32) {
+        const int ly = j / pw, lx = j - ly * pw;
+        const uint8_t* row = s_in + ly * iw + lx;
+        float acc = 0.0f;
+#pragma unroll
+        for (int q = 0; q <= 2 * D6_RB; ++q) acc = fadd(acc, fmul(a.btaps[q], static_cast<float>(row[q])));
+        s_tmp[j] = acc;
+    }
+    __syncwarp();
+    // vertical pass at the sample points + ternary tests -> gt / lt bitplanes
+    auto S = [&](int x, int y) {  // patch coordinates in [-P, P]
+        const float* col = s_tmp + (P + y) * pw + (P + x);
+        float acc = 0.0f;
+#pragma unroll
+        for (int q = 0; q <= 2 * D6_RB; ++q) acc = fadd(acc, fmul(a.btaps[q], col[q * pw]));
+        return acc;
+    };
+    const int W = (a.n_d + 63) / 64;
+    uint64_t* d = a.desc_out + (static_cast<size_t>(rg.out_slot) * a.cap_slot + idx) * 2 * W;
+    for (int w = 0; w < W; ++w) {
+        unsigned g[2], l[2];
+        for (int h = 0; h < 2; ++h) {
+            const int pi = w * 64 + h * 32 + lane;
+            bool gt = false, lt = false;
+            if (pi < a.n_d) {
+                const lp_pair pr = s_pairs[pi];
+                const float ip = S(pr.px, pr.py), iq = S(pr.qx, pr.qy);
+                gt = ip > iq;
+                lt = ip < iq;
+            }
+            g[h] = __ballot_sync(0xffffffffu, gt);
+            l[h] = __ballot_sync(0xffffffffu, lt);
+        }
+        if (lane == 0) {
+            d[w] = static_cast<uint64_t>(g[0]) | (static_cast<uint64_t>(g[1]) << 32);
+            d[W + w] = static_cast<uint64_t>(l[0]) | (static_cast<uint64_t>(l[1]) << 32);
+        }
+    }
+    if (lane == 0) a.kp_out[static_cast<size_t>(rg.out_slot) * a.cap_slot + idx] = kp;
+}
+
 void extract_launch(const ExtractArgs& a, cudaStream_t s) {
     if (a.nregions == 0) return;
     LPB_CUDA(cudaMemsetAsync(a.surv_count, 0, sizeof(unsigned) * a.nregions, s));
@@ -762,6 +871,18 @@ void extract_launch(const ExtractArgs& a, cudaStream_t s) {
     }
     const int P = a.patch_half, RB = a.blur_r;
     const int pw = 2 * P + 1, iw = pw + 2 * RB;
+    if (RB == D6_RB) {
+        const int warp_bytes6 = (((iw * iw + 15) & ~15) + iw * pw * 4 + 15) & ~15;
+        const int head6 = (a.n_d * static_cast<int>(sizeof(lp_pair)) + 15) & ~15;
+        int warps6 = 8;
+        while (warps6 > 1 && head6 + warps6 * warp_bytes6 > 200 * 1024) warps6 >>= 1;
+        const int smem6 = head6 + warps6 * warp_bytes6;
+        // one profiler key for both implementations (k_describe/0)
+        auto* k_describe = &k_describe6;
+        LPB_CUDA(cudaFuncSetAttribute(k_describe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem6));
+        LPB_LAUNCH(k_describe, cdiv(a.nregions * a.top_n, warps6), warps6 * 32, smem6, s, a, warp_bytes6);
+        return;
+    }
     const int warp_bytes = (((iw * iw + 15) & ~15) + (iw * pw + pw * pw) * 4 + 15) & ~15;
     const int head = (a.n_d * static_cast<int>(sizeof(lp_pair)) + (2 * kMaxBlurR + 1) * 4 + 15) & ~15;
     int warps = 8;

@@ -41,6 +41,7 @@ struct ExtractArgs {
     lp_keypoint* kp_region;  // nregions * top_n
     int* count_region;       // nregions
     const float* blur_taps;  // 2*RB+1
+    float btaps[2 * kMaxBlurR + 1];  // the same taps in the parameter bank
     int blur_r;
     const lp_pair* pairs;
     int n_d, patch_half;

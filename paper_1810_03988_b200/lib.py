@@ -13,7 +13,8 @@ from . import abi
 from .api import AbiWrapper, _ptr
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "liblorbpano_b200.so")
+# LPB_LIB selects an alternative build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("LPB_LIB") or os.path.join(HERE, "_lib", "liblorbpano_b200.so")
 CSRC = os.path.join(HERE, "csrc")
 
 _lock = threading.Lock()
