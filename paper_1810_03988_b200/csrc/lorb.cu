@@ -249,7 +249,7 @@ __device__ __forceinline__ uint32_t arc9(const uint32_t (&f)[16]) {
 }
 }  // namespace d9
 
-__global__ void __launch_bounds__(256, 3) k_detect9(const __grid_constant__ ExtractArgs a) {
+__global__ void __launch_bounds__(256, 4) k_detect9(const __grid_constant__ ExtractArgs a) {
     using namespace d9;
     __shared__ uint32_t s_img[SH * SWW];
     __shared__ int s_grad[GY * GX];  // (gx & 0xffff) | gy << 16
@@ -324,7 +324,9 @@ __global__ void __launch_bounds__(256, 3) k_detect9(const __grid_constant__ Extr
                 for (int q = 0; q < 3; ++q) wv[dy][q] = w0[dy * SWW + q];
             const uint32_t C = wv[3][1];
             const uint32_t Hc = __vaddus4(C, T4), Lc = __vsubus4(C, T4);
-            uint32_t fb[16], fd[16];
+            // brighter flag in bit 7, darker flag in bit 6 of every byte: one
+            // AND/OR arc network tests both runs at once
+            uint32_t fc[16];
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
                 const int dx = ring_dx(k), dy = ring_dy(k) + 3;
@@ -335,10 +337,10 @@ __global__ void __launch_bounds__(256, 3) k_detect9(const __grid_constant__ Extr
                     v = __byte_perm(wv[dy][1], wv[dy][2], dx | (dx + 1) << 4 | (dx + 2) << 8 | (dx + 3) << 12);
                 else
                     v = __byte_perm(wv[dy][0], wv[dy][1], (4 + dx) | (5 + dx) << 4 | (6 + dx) << 8 | (7 + dx) << 12);
-                fb[k] = gt_u8(v, Hc);
-                fd[k] = gt_u8(Lc, v);
+                fc[k] = (gt_u8(v, Hc) & 0x80808080u) | ((gt_u8(Lc, v) >> 1) & 0x40404040u);
             }
-            uint32_t F = (arc9(fb) | arc9(fd)) & 0x80808080u;
+            uint32_t F = arc9(fc) & 0xC0C0C0C0u;
+            F = (F | (F << 1)) & 0x80808080u;
             // scan area (lorb.hpp:196-198) and the tile + ring
             const int y = oy - 1 + r, x4 = fx0 + 4 * j;
             if (!valid || y < rg.y0 || y >= rg.y1) F = 0;
