@@ -72,7 +72,7 @@ def run_streams(args, cfgd, lp, world, rank, local, dist):
         rig = Rig(lp, 2, w, h, p)
         rigs.append(rig)
         panos.append(torch.empty(rig.panorama_capacity(), dtype=torch.uint8, device="cuda"))
-    nthreads = min(len(rigs), 16)
+    nthreads = min(len(rigs), int(os.environ.get("LPB_CFG5_THREADS", "32")))
     groups = [list(range(i, len(rigs), nthreads)) for i in range(nthreads)]
 
     def run(steps, base):

@@ -9,7 +9,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cstdio>
+#include <mutex>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -56,6 +58,41 @@ struct DevImage {
     int w, h;
 };
 constexpr int kMaxCams = 64;
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
+// and size, not per launch: concurrent rigs on one device then never meet in
+// the driver's attribute path.
+inline void ensure_dyn_smem(const void* kernel, int bytes) {
+    struct Slot {
+        std::atomic<const void*> fn{nullptr};
+        std::atomic<int> bytes[16];
+    };
+    static Slot slots[64];
+    static std::mutex mu;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dev &= 15;
+    for (auto& sl : slots) {
+        const void* f = sl.fn.load(std::memory_order_acquire);
+        if (f == kernel) {
+            if (sl.bytes[dev].load(std::memory_order_acquire) >= bytes) return;
+            break;
+        }
+        if (f == nullptr) break;
+    }
+    std::lock_guard<std::mutex> l(mu);
+    for (auto& sl : slots) {
+        const void* f = sl.fn.load(std::memory_order_acquire);
+        if (f != nullptr && f != kernel) continue;
+        if (sl.bytes[dev].load() >= bytes) return;
+        const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (e != cudaSuccess) throw Status(LP_CUDA_ERROR, std::string("cudaFuncSetAttribute -> ") + cudaGetErrorString(e));
+        sl.bytes[dev].store(bytes, std::memory_order_release);
+        sl.fn.store(kernel, std::memory_order_release);
+        return;
+    }
+    throw Status(LP_INTERNAL, "ensure_dyn_smem: slot table full");
+}
 
 // device-side status word: first error wins (atomicCAS from 0)
 __device__ __forceinline__ void dev_fail(int* status, int code) {

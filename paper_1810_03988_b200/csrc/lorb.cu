@@ -868,7 +868,7 @@ void extract_launch(const ExtractArgs& a, cudaStream_t s) {
         LPB_LAUNCH(k_topn, a.nregions, 1024, 0, s, a);
     } else {
         const int topn_smem = kTopnSortCap * sizeof(uint64_t);
-        LPB_CUDA(cudaFuncSetAttribute(k_topn_radix, cudaFuncAttributeMaxDynamicSharedMemorySize, topn_smem));
+        ensure_dyn_smem(reinterpret_cast<const void*>(k_topn_radix), topn_smem);
         LPB_LAUNCH(k_topn_radix, a.nregions, 1024, topn_smem, s, a);
     }
     const int P = a.patch_half, RB = a.blur_r;
@@ -881,7 +881,7 @@ void extract_launch(const ExtractArgs& a, cudaStream_t s) {
         const int smem6 = head6 + warps6 * warp_bytes6;
         // one profiler key for both implementations (k_describe/0)
         auto* k_describe = &k_describe6;
-        LPB_CUDA(cudaFuncSetAttribute(k_describe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem6));
+        ensure_dyn_smem(reinterpret_cast<const void*>(k_describe), smem6);
         LPB_LAUNCH(k_describe, cdiv(a.nregions * a.top_n, warps6), warps6 * 32, smem6, s, a, warp_bytes6);
         return;
     }
@@ -891,7 +891,7 @@ void extract_launch(const ExtractArgs& a, cudaStream_t s) {
     while (warps > 1 && head + warps * warp_bytes > 200 * 1024) warps >>= 1;
     const int smem = head + warps * warp_bytes;
     if (smem > 227 * 1024) throw Status(LP_BAD_PARAMS, "describe: patch too large for shared memory");
-    LPB_CUDA(cudaFuncSetAttribute(k_describe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ensure_dyn_smem(reinterpret_cast<const void*>(k_describe), smem);
     const int total = a.nregions * a.top_n;
     LPB_LAUNCH(k_describe, cdiv(total, warps), warps * 32, smem, s, a, warp_bytes);
 }

@@ -191,7 +191,7 @@ void match_launch(const MatchArgs& a, cudaStream_t s) {
     int p2 = 1;
     while (p2 < a.cap) p2 <<= 1;
     const int smem = p2 * 4;
-    LPB_CUDA(cudaFuncSetAttribute(k_match_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ensure_dyn_smem(reinterpret_cast<const void*>(k_match_finalize), smem);
     LPB_LAUNCH(k_match_finalize, a.npairs, 1024, smem, s, a);
 }
 
