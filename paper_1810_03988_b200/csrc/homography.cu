@@ -325,17 +325,19 @@ struct RefitShared {
     int status;
 };
 
-// dlt_homography over p[idx[0..m)] (block-wide). Scratch: A 2m x 9, vbuf 2m,
-// terms 2m. Returns the status on every thread; H valid on every thread.
+// dlt_homography over p[idx[0..m)] (p[0..m) when idx is null), block-wide.
+// Scratch (shared or global): A 2m x 9, vbuf 2m, terms 2m. Returns the status
+// on every thread; H valid on every thread.
 __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, double* vbuf, double* terms,
                          double* H, RefitShared& sh) {
     const int tid = threadIdx.x;
+    auto P = [&](int i) -> const lp_corr& { return idx ? p[idx[i]] : p[i]; };
     if (tid == 0) {
         sh.status = LP_OK;
         if (m < 4) sh.status = LP_INSUFFICIENT_MATCHES;
         if (m == 4) {
             lp_corr q[4];
-            for (int i = 0; i < 4; ++i) q[i] = p[idx[i]];
+            for (int i = 0; i < 4; ++i) q[i] = P(i);
             for (int i = 0; i < 4 && sh.status == LP_OK; ++i)
                 for (int j = i + 1; j < 4; ++j)
                     for (int k = j + 1; k < 4; ++k) {
@@ -347,7 +349,7 @@ __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, dou
         // hartley_normalizer centroids: sequential sums (homography.hpp:83-88)
         Norm ns{0, 0, 1}, nd{0, 0, 1};
         for (int i = 0; i < m; ++i) {
-            const lp_corr c = p[idx[i]];
+            const lp_corr c = P(i);
             ns.cx += c.sx;
             ns.cy += c.sy;
             nd.cx += c.dx;
@@ -365,7 +367,7 @@ __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, dou
     {
         const Norm ns = sh.ns, nd = sh.nd;
         for (int i = tid; i < m; i += blockDim.x) {  // distance terms, in parallel
-            const lp_corr c = p[idx[i]];
+            const lp_corr c = P(i);
             double x = c.sx - ns.cx, y = c.sy - ns.cy;
             terms[i] = sqrt(x * x + y * y);
             x = c.dx - nd.cx;
@@ -387,7 +389,7 @@ __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, dou
     const Norm ns = sh.ns, nd = sh.nd;
     const int rows = 2 * m;
     for (int i = tid; i < m; i += blockDim.x) {
-        const lp_corr c = p[idx[i]];
+        const lp_corr c = P(i);
         const double x = (c.sx - ns.cx) * ns.scale, y = (c.sy - ns.cy) * ns.scale;
         const double u = (c.dx - nd.cx) * nd.scale, v = (c.dy - nd.cy) * nd.scale;
         double* r0 = A + static_cast<size_t>(2 * i) * 9;
@@ -642,7 +644,21 @@ __global__ void __launch_bounds__(256) k_prosac(ProsacArgs a) {
     }
     const int n_in = block_compact(n, idx, [&](int i) { return ste(bh, bhi, m[i]) <= a.threshold; });
     double Hr[9], Hri[9];
-    const int st = dlt_block(m, idx, n_in, A, vbuf, terms, Hr, S.refit);
+    int st;
+    if (n_in <= a.smem_rows) {
+        // the inliers and the whole refit system in shared memory: the
+        // sequential Hartley sums and the blocked QR passes read on-chip
+        extern __shared__ __align__(16) double s_refit[];
+        double* sA = s_refit;                                        // 2 n_in x 9
+        double* sv = sA + static_cast<size_t>(2 * a.smem_rows) * 9;  // 2 n_in
+        double* st_terms = sv + 2 * a.smem_rows;                     // 2 n_in
+        lp_corr* sc = reinterpret_cast<lp_corr*>(st_terms + 2 * a.smem_rows);
+        for (int i = tid; i < n_in; i += blockDim.x) sc[i] = m[idx[i]];
+        __syncthreads();
+        st = dlt_block(sc, nullptr, n_in, sA, sv, st_terms, Hr, S.refit);
+    } else {
+        st = dlt_block(m, idx, n_in, A, vbuf, terms, Hr, S.refit);
+    }
     if (tid == 0) {
         S.refit_ok = st == LP_OK && h_inverse(Hr, Hri);
         for (int i = 0; i < 9; ++i) {
@@ -675,9 +691,13 @@ __global__ void __launch_bounds__(256) k_prosac(ProsacArgs a) {
     }
 }
 
-void prosac_launch(const ProsacArgs& a, cudaStream_t s) {
-    if (a.npairs <= 0) return;
-    LPB_LAUNCH(k_prosac, a.npairs, 256, 0, s, a);
+void prosac_launch(const ProsacArgs& a0, cudaStream_t s) {
+    ProsacArgs a = a0;
+    // refit rows kept on chip: 2 rows x 9 + 2 + 2 doubles and one lp_corr per inlier
+    a.smem_rows = std::min(a.cap, kRefitSmemRows);
+    const int smem = a.smem_rows * static_cast<int>(2 * 9 * 8 + 2 * 8 + 2 * 8 + sizeof(lp_corr));
+    ensure_dyn_smem(reinterpret_cast<const void*>(&k_prosac), smem);
+    LPB_LAUNCH(k_prosac, a.npairs, 256, smem, s, a);
 }
 
 __global__ void k_chain(const lp_homography* ph, const int* pst, int npairs, lp_homography* chain,

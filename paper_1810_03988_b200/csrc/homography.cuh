@@ -26,7 +26,10 @@ struct ProsacArgs {
     int* trace_pool;            // npairs * max_iter (optional)
     int* trace_samples;         // npairs * max_iter * 4 (optional)
     int* pair_status;           // npairs: in = upstream status (0 ok), out = PROSAC status
+    int smem_rows;              // set by prosac_launch: refits with <= this many inliers run in shared memory
 };
+
+constexpr int kRefitSmemRows = 800;  // 800 x 232 B = 186 KB of dynamic shared memory
 
 // scratch doubles per pair: refit system A (2cap x 9), Householder vector
 // (2cap), Hartley distance terms (2cap), inlier index list (cap ints)
