@@ -138,18 +138,31 @@ __device__ void warp_jacobi_null(double (&rr)[9], double (&hv)[9]) {
                 be[kk] = tree9(rr[q] * rr[q]);
                 ga[kk] = tree9(rr[p] * rr[q]);
             }
+            // the four rotations' scalar work (divisions, square roots) runs
+            // once, on lanes 0..3 in parallel, instead of four times in series
+            // on every lane; (c, s) are then broadcast. Same formulas, same
+            // rounding: lane kk computes exactly what every lane computed.
+            const int kr = lane & 3;
+            const double alk = kr == 0 ? al[0] : kr == 1 ? al[1] : kr == 2 ? al[2] : al[3];
+            const double bek = kr == 0 ? be[0] : kr == 1 ? be[1] : kr == 2 ? be[2] : be[3];
+            const double gak = kr == 0 ? ga[0] : kr == 1 ? ga[1] : kr == 2 ? ga[2] : ga[3];
+            const bool skip = gak == 0.0 || gak * gak <= eps2 * (alk * bek) ||
+                              fabs(gak) <= 2.220446049250313e-16 * fmax(alk, bek);
+            double ck = 1.0, sk = 0.0;
+            if (!skip) {
+                const double zeta = (bek - alk) / (2.0 * gak);
+                const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                ck = 1.0 / sqrt(1.0 + t * t);
+                sk = ck * t;
+            }
+            const unsigned rot = __ballot_sync(kFull, !skip) & 0xFu;
+            if (rot) rotated = true;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
                 const int a0 = (rnd + kk + 1) % 9, b0 = (rnd - kk - 1 + 9) % 9;
                 const int p = a0 < b0 ? a0 : b0, q = a0 < b0 ? b0 : a0;
-                if (ga[kk] == 0.0 || ga[kk] * ga[kk] <= eps2 * (al[kk] * be[kk]) ||
-                    fabs(ga[kk]) <= 2.220446049250313e-16 * fmax(al[kk], be[kk]))
-                    continue;
-                rotated = true;
-                const double zeta = (be[kk] - al[kk]) / (2.0 * ga[kk]);
-                const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                const double c = 1.0 / sqrt(1.0 + t * t);
-                const double s = c * t;
+                const double c = __shfl_sync(kFull, ck, kk), s = __shfl_sync(kFull, sk, kk);
+                if (!((rot >> kk) & 1u)) continue;
                 const double up = rr[p], uq = rr[q];
                 rr[p] = c * up - s * uq;
                 rr[q] = s * up + c * uq;
@@ -501,7 +514,7 @@ struct ProsacShared {
     RefitShared refit;
 };
 
-__global__ void __launch_bounds__(256) k_prosac(ProsacArgs a) {
+__global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
     __shared__ ProsacShared S;
     const int pair = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
