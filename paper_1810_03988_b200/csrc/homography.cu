@@ -50,6 +50,49 @@ __device__ uint64_t mt_next(Mt64& r) {
     y ^= y >> 43;
     return y;
 }
+// the first twist of a freshly seeded state by one warp: the serial loop's
+// data flow is three parallel phases (i < 156 reads only old words; 156 <= i
+// < 311 reads old words and the new words i-156; i = 311 reads new words 0
+// and 155), so the resulting state is the serial one exactly
+__device__ void mt_twist_warp(Mt64& r) {
+    const int lane = threadIdx.x & 31;
+    auto step = [&](int i) {
+        const uint64_t x = (r.mt[i] & 0xFFFFFFFF80000000ull) | (r.mt[(i + 1) % 312] & 0x7FFFFFFFull);
+        uint64_t xa = x >> 1;
+        if (x & 1ull) xa ^= 0xB5026F5AA96619E9ull;
+        return r.mt[(i + 156) % 312] ^ xa;
+    };
+    uint64_t v[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = lane + 32 * k;
+        if (i < 156) v[k] = step(i);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = lane + 32 * k;
+        if (i < 156) r.mt[i] = v[k];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = 156 + lane + 32 * k;
+        if (i < 311) v[k] = step(i);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int i = 156 + lane + 32 * k;
+        if (i < 311) r.mt[i] = v[k];
+    }
+    __syncwarp();
+    if (lane == 0) {
+        r.mt[311] = step(311);
+        r.idx = 0;
+    }
+    __syncwarp();
+}
 __device__ int uid_int(Mt64& r, int a, int b) {
     const uint64_t range = static_cast<uint64_t>(static_cast<int64_t>(b)) -
                            static_cast<uint64_t>(static_cast<int64_t>(a)) + 1ull;
@@ -293,7 +336,9 @@ __device__ int dlt_minimal_warp(const lp_corr* p, double* H) {
 // canonical blocked dot products (oracle/shim/Eigen/Dense dot_blocked): lane
 // l = row & 255 accumulates rows in increasing order, then the pairwise tree
 // p[l] += p[l+s], s = 128..1 (s >= 32 in shared memory, s <= 16 by shuffles)
-template <int K>
+// SELF: column 0 is v itself (v.v beside the v.col_k, one pass, each in the
+// same canonical order as its own call)
+template <int K, bool SELF = false>
 __device__ void block_dots(const double* v, int sv, const double* const* cols, int sc, int r0,
                            int r1, double (*s_red)[256], double* out) {
     const int l = threadIdx.x;
@@ -304,8 +349,12 @@ __device__ void block_dots(const double* v, int sv, const double* const* cols, i
     for (int i = i0; i < r1; i += 256) {
         const double vi = v[static_cast<size_t>(i) * sv];
 #pragma unroll
-        for (int k = 0; k < K; ++k)
-            if (cols[k]) p[k] = p[k] + vi * cols[k][static_cast<size_t>(i) * sc];
+        for (int k = 0; k < K; ++k) {
+            if (SELF && k == 0)
+                p[0] = p[0] + vi * vi;
+            else if (cols[k])
+                p[k] = p[k] + vi * cols[k][static_cast<size_t>(i) * sc];
+        }
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) s_red[k][l] = p[k];
@@ -331,7 +380,7 @@ __device__ void block_dots(const double* v, int sv, const double* const* cols, i
 }
 
 struct RefitShared {
-    double red[8][256];
+    double red[9][256];
     double r[81];
     double H[9];
     Norm ns, nd;
@@ -426,13 +475,15 @@ __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, dou
             for (int i = tid; i < rows; i += blockDim.x)
                 vbuf[i] = i < j ? 0.0 : (i == j ? alpha - beta : A[static_cast<size_t>(i) * 9 + j]);
             __syncthreads();
-            const double* cv[1] = {vbuf};
-            double vn2;
-            block_dots<1>(vbuf, 1, cv, 1, j, rows, sh.red, &vn2);
-            const double* ck[8];
-            for (int k = 0; k < 8; ++k) ck[k] = (j + 1 + k < 9) ? A + j + 1 + k : nullptr;
+            // v.v and v.A_k (k > j) in one pass
+            const double* ck[9];
+            ck[0] = vbuf;
+            for (int k = 0; k < 8; ++k) ck[k + 1] = (j + 1 + k < 9) ? A + j + 1 + k : nullptr;
+            double vd[9];
+            block_dots<9, true>(vbuf, 1, ck, 9, j, rows, sh.red, vd);
+            const double vn2 = vd[0];
             double dk[8];
-            block_dots<8>(vbuf, 1, ck, 9, j, rows, sh.red, dk);
+            for (int k = 0; k < 8; ++k) dk[k] = vd[k + 1];
             double f[8];
             for (int k = 0; k < 8; ++k) f[k] = 2.0 * dk[k] / vn2;
             for (int i = j + tid; i < rows; i += blockDim.x) {
@@ -545,6 +596,9 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
         S.done = 0;
         for (int i = 0; i < 9; ++i) S.best_h[i] = (i % 4 == 0) ? 1.0 : 0.0;
     }
+    __syncthreads();
+    if (warp == 0) mt_twist_warp(S.rng);  // the first draw's twist, in parallel
+    __syncthreads();
     const int* exit_row = a.exit_tab + (a.nmax > 0 ? static_cast<size_t>(n) * (a.nmax + 1) : 0);
     for (int t0 = 1; t0 <= a.max_iter; t0 += kChunk) {
         const int chunk = min(kChunk, a.max_iter - t0 + 1);
