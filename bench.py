@@ -479,16 +479,19 @@ def main():
         achieved = byts / (avg * 1e-3) / 1e9 if byts > 0 else None
         # DRAM bytes of the same launch from the committed ncu --set full capture
         # (scripts/ncu_traffic.py -> profiles/ncu_traffic.json), or null
-        traffic = None
+        traffic, limiter = None, None
         try:
             nj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
             traffic = nj.get(args.config, {}).get(dom, {}).get("traffic_bytes")
+            limiter = nj.get(args.config, {}).get(dom, {}).get("limiter")
         except Exception:
             pass
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                     "peak_source": peak_src, "unit": "GB/s",
                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                     "algorithmic_bytes_per_launch": byts, "avg_launch_ms": avg,
+                    # what does bound it (same ncu capture): issue slots / FP64 pipe / DRAM
+                    "ncu_limiter": limiter,
                     "share_of_kernel_time": kern[dom][0] / max(1e-9, sum(v[0] for v in kern.values()))}
         stage = {k: round(v[0] / v[1], 4) for k, v in sorted(kern.items(), key=lambda kv: -kv[1][0])}
         stage["_kernel_ms_per_frame"] = round(step_ms, 4)

@@ -4,7 +4,7 @@ DRAM traffic, throughput fractions, pipe utilisation, occupancy."""
 import csv
 import sys
 
-COLS = [("time_us", "gpu__time_duration.sum", 1e-3),
+COLS = [("time_us", "gpu__time_duration.sum", 1),
         ("dram_rd_MB", "dram__bytes_read.sum", 1e-6), ("dram_wr_MB", "dram__bytes_write.sum", 1e-6),
         ("dram%", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1),
         ("sm%", "sm__throughput.avg.pct_of_peak_sustained_elapsed", 1),

@@ -10,7 +10,7 @@ import json
 import os
 import sys
 
-FAMILY = {"k_detect9": "k_detect", "k_detect": "k_detect", "k_pyr_down2": "k_pyr_down",
+FAMILY = {"k_detect9": "k_detect", "k_detect": "k_detect", "k_pyr_down2": "k_pyr_down", "k_describe6": "k_describe",
           "k_blend_lean": "k_blend_level", "k_blend_level": "k_blend_level"}
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
         "msecond": 1e-3, "second": 1}
@@ -30,18 +30,25 @@ def main(path, cfg, frames=None):
         def val(m):
             i = ix[m]
             return float(r[i].replace(",", "")) * UNIT.get(units[i], 1)
+        def opt(m):
+            return val(m) if m in ix and r[ix[m]] else None
         launches.append((fam, val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
-                         val("gpu__time_duration.sum")))
+                         val("gpu__time_duration.sum"),
+                         {"issue_active_pct": opt("sm__inst_issued.avg.pct_of_peak_sustained_active"),
+                          "fp64_pipe_pct": opt("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                          "dram_pct": opt("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                          "warps_active_pct": opt("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                          "registers": opt("launch__registers_per_thread")}))
     per = collections.defaultdict(list)
-    for fam, b, t in launches:
-        per[fam].append((b, t))
+    for fam, b, t, lim in launches:
+        per[fam].append((b, t, lim))
     if frames is None:
         frames = max(1, len(per.get("k_detect", [])))
     out = {}
     for fam, lst in per.items():
         n = max(1, len(lst) // frames)
-        for occ, (b, t) in enumerate(lst[-n:]):
-            out[f"{fam}/{occ}"] = {"traffic_bytes": b, "ncu_us": t * 1e6}
+        for occ, (b, t, lim) in enumerate(lst[-n:]):
+            out[f"{fam}/{occ}"] = {"traffic_bytes": b, "ncu_us": t * 1e6, "limiter": lim}
     dst = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
     allj = json.load(open(dst)) if os.path.exists(dst) else {}
     allj[cfg] = out
