@@ -381,3 +381,36 @@ def test_rig_frames_in_flight(lp, orc, params):
         W, H, _, _ = rig.wait(tk)
         got = host[t][:W * H].numpy().reshape(H, W)
         assert np.array_equal(got, want[t]), t
+
+
+def test_concurrent_rigs_threads(lp, orc):
+    """Independent rigs on one context, driven from host threads (the config-5
+    shape): each rig has its own stage stream, so their frames overlap on the
+    device; every panorama must equal the oracle's for that rig's input."""
+    import threading
+
+    from paper_1810_03988_b200 import Rig
+    p = orc.default_params()
+    p.seed = p.matching.seed = 42
+    nrig, frames = 6, 3
+    inputs = [orc.planted_pair(320, 240, 0.25, 100 + i)[:2] for i in range(nrig)]
+    want = [orc.stitch_frame(list(inputs[i]), p, frame_index=0)["panorama"] for i in range(nrig)]
+    rigs = [Rig(lp, 2, 320, 240, p) for _ in range(nrig)]
+    got = [[None] * frames for _ in range(nrig)]
+    errs = []
+
+    def run(i):
+        try:
+            for f in range(frames):
+                got[i][f] = rigs[i].stitch(list(inputs[i]), f)["panorama"]
+        except Exception as e:  # surfaced below
+            errs.append(e)
+    ths = [threading.Thread(target=run, args=(i,)) for i in range(nrig)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errs, errs
+    for i in range(nrig):
+        for f in range(frames):
+            assert np.array_equal(got[i][f], want[i]), (i, f)
