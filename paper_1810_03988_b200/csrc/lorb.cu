@@ -516,10 +516,14 @@ __global__ void __launch_bounds__(1024) k_topn(ExtractArgs a) {
             const int dbits = pbits + 8 <= 64 ? 8 : 64 - pbits;
             for (int i = tid; i < 256; i += blockDim.x) s_hist[i] = 0;
             __syncthreads();
-            for (int i = tid; i < n; i += blockDim.x) {
-                const uint64_t k = keys[i];
-                if ((k >> (64 - pbits)) == prefix)
-                    atomicAdd(&s_hist[(k >> (64 - pbits - dbits)) & ((1u << dbits) - 1u)], 1u);
+            for (int i0 = tid; i0 < n; i0 += 8 * 1024) {  // 8 keys in flight per thread
+                uint64_t kk[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) kk[u] = i0 + 1024 * u < n ? __ldg(keys + i0 + 1024 * u) : 0ull;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (i0 + 1024 * u < n && (kk[u] >> (64 - pbits)) == prefix)
+                        atomicAdd(&s_hist[(kk[u] >> (64 - pbits - dbits)) & ((1u << dbits) - 1u)], 1u);
             }
             __syncthreads();
             if (tid == 0) {
@@ -543,12 +547,16 @@ __global__ void __launch_bounds__(1024) k_topn(ExtractArgs a) {
         __syncthreads();
         const uint64_t prefix = s_prefix;
         const int sh = 64 - s_pbits;
-        for (int i = tid; i < n; i += blockDim.x) {
-            const uint64_t k = keys[i];
-            if ((sh == 64 ? 0 : (k >> sh)) >= prefix) {
-                const int slot = atomicAdd(&s_m, 1);
-                if (slot < kTopnRankCap) s_keys[slot] = k;
-            }
+        for (int i0 = tid; i0 < n; i0 += 8 * 1024) {  // 8 keys in flight per thread
+            uint64_t kk[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) kk[u] = i0 + 1024 * u < n ? __ldg(keys + i0 + 1024 * u) : 0ull;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (i0 + 1024 * u < n && (sh == 64 ? 0 : (kk[u] >> sh)) >= prefix) {
+                    const int slot = atomicAdd(&s_m, 1);
+                    if (slot < kTopnRankCap) s_keys[slot] = kk[u];
+                }
         }
         __syncthreads();
         m = min(s_m, kTopnRankCap);
