@@ -821,14 +821,23 @@ __global__ void __launch_bounds__(256) k_describe6(const __grid_constant__ Extra
             if (j0 + 32 * u < iw * iw) s_in[j0 + 32 * u] = v[u];
     }
     __syncwarp();
-    // horizontal pass: every staged row, the pw patch columns
-    for (int j = lane; j < iw * pw; j += 32) {
-        const int ly = j / pw, lx = j - ly * pw;
+    // horizontal pass: every staged row, the pw patch columns, two adjacent
+    // columns per lane (14 staged pixels converted once for both sums)
+    const int pw2 = (pw + 1) / 2;
+    for (int j = lane; j < iw * pw2; j += 32) {
+        const int ly = j / pw2, lx = 2 * (j - ly * pw2);
         const uint8_t* row = s_in + ly * iw + lx;
-        float acc = 0.0f;
+        float v[2 * D6_RB + 2];
 #pragma unroll
-        for (int q = 0; q <= 2 * D6_RB; ++q) acc = fadd(acc, fmul(a.btaps[q], static_cast<float>(row[q])));
-        s_tmp[j] = acc;
+        for (int q = 0; q < 2 * D6_RB + 2; ++q) v[q] = lx + q < iw ? static_cast<float>(row[q]) : 0.0f;
+        float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+        for (int q = 0; q <= 2 * D6_RB; ++q) {
+            a0 = fadd(a0, fmul(a.btaps[q], v[q]));
+            a1 = fadd(a1, fmul(a.btaps[q], v[q + 1]));
+        }
+        s_tmp[ly * pw + lx] = a0;
+        if (lx + 1 < pw) s_tmp[ly * pw + lx + 1] = a1;
     }
     __syncwarp();
     // vertical pass at the sample points + ternary tests -> gt / lt bitplanes
