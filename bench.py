@@ -504,7 +504,7 @@ def main():
         # pinned host frames in, pinned host panoramas out, 3 frames in flight
         # (lp_rig_submit / lp_rig_wait): every step's ingest copy, stages and
         # panorama egress are inside the timed region
-        depth = 3
+        depth = int(os.environ.get("LPB_E2E_DEPTH", "3"))
         host_sets = [[torch.from_numpy(c).pin_memory() for c in s] for s in sets[:2]]
         hpanos = [torch.empty(pano_cap, dtype=torch.uint8).pin_memory() for _ in range(depth)]
 
