@@ -109,8 +109,8 @@ def run_streams(args, cfgd, lp, world, rank, local, dist):
     clk = clocks.stop()
     launches = kernel_launches() - n0
     csum = sum(int(pb[:1 << 20].to(torch.int64).sum().item()) for pb in panos)
-    ms_max, frames, checksums = gather_results(RankResult(args.steps * len(rigs), el_ms, csum),
-                                               torch.device("cuda", local))
+    coll_dev = torch.device("cuda", local) if dist is None or dist.get_backend() == "nccl" else torch.device("cpu")
+    ms_max, frames, checksums = gather_results(RankResult(args.steps * len(rigs), el_ms, csum), coll_dev)
     if rank == 0:
         line = {"metric": METRIC, "value": aggregate_fps(frames, ms_max), "unit": "frames/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -385,11 +385,21 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # LPB_RANKS_ON_ONE_GPU=1 (+ LPB_DIST_BACKEND=gloo): every rank on cuda:0, a
+    # single-GPU rehearsal of the multi-rank path (tests/gpu_multirank); the
+    # driver's runs use one GPU per rank over NCCL
+    if os.environ.get("LPB_RANKS_ON_ONE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("LPB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    coll_dev = torch.device("cuda", local) if dist is None or dist.get_backend() == "nccl" else torch.device("cpu")
 
     from paper_1810_03988_b200 import Lorb, Rig, abi, frame_out, kernel_launches, load
     from paper_1810_03988_b200.shard import RankResult, aggregate_fps, gather_results
@@ -441,8 +451,7 @@ def main():
     # panorama checksums (paper_1810_03988_b200.shard)
     pano = dpano[:canvas[0] * canvas[1]]
     csum = int(pano.to(torch.int64).sum().item())
-    ms_max, total_frames, checksums = gather_results(RankResult(args.steps, ms, csum),
-                                                     torch.device("cuda", local))
+    ms_max, total_frames, checksums = gather_results(RankResult(args.steps, ms, csum), coll_dev)
     value = aggregate_fps(total_frames, ms_max)
 
     # ---- per-kernel profile pass (same workload; events around every launch)
@@ -523,7 +532,7 @@ def main():
         t0 = time.perf_counter()
         run_e2e(args.steps, 30_000)
         el = time.perf_counter() - t0
-        tt = torch.tensor([el], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([el], dtype=torch.float64, device=coll_dev)
         if dist is not None:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         got = hpanos[(args.steps - 1) % depth][:canvas[0] * canvas[1]].to(torch.int64).sum().item()
