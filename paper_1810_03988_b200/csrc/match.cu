@@ -55,7 +55,7 @@ __device__ __forceinline__ void top2_insert(int d, int j, int& d0, int& j0, int&
     }
 }
 
-constexpr int kQueriesPerWarp = 4;
+constexpr int kQueriesPerWarp = 1;
 constexpr int kMaxW = 8;  // n_d <= 512
 
 __global__ void __launch_bounds__(256) k_match_query(MatchArgs a) {
