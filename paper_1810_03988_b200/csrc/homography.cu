@@ -359,16 +359,17 @@ __device__ void block_dots(const double* v, int sv, const double* const* cols, i
 #pragma unroll
     for (int k = 0; k < K; ++k) s_red[k][l] = p[k];
     __syncthreads();
-    for (int s = 128; s >= 32; s >>= 1) {
-        if (l < s)
-#pragma unroll
-            for (int k = 0; k < K; ++k) s_red[k][l] = s_red[k][l] + s_red[k][l + s];
-        __syncthreads();
-    }
+    // the canonical tree p[l] += p[l + s], s = 128, 64, 32, then shuffles
+    // 16..1, all in warp 0 (lane l owns partial sums l, l+32, l+64, l+96):
+    // the same additions in the same order with one barrier instead of four
     if (l < 32) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            double x = s_red[k][l];
+            const double a0 = s_red[k][l] + s_red[k][l + 128];
+            const double a1 = s_red[k][l + 32] + s_red[k][l + 160];
+            const double a2 = s_red[k][l + 64] + s_red[k][l + 192];
+            const double a3 = s_red[k][l + 96] + s_red[k][l + 224];
+            double x = (a0 + a2) + (a1 + a3);
             for (int s = 16; s >= 1; s >>= 1) x = x + __shfl_down_sync(kFull, x, s);
             if (l == 0) s_red[k][0] = x;
         }
