@@ -318,6 +318,9 @@ void* lp_rig_stream(lp_rig* rig);
 /* Frame scheduler: 2 (default) runs extraction on a second stream concurrently
  * with warp/blend on cached-homography frames; 1 runs every stage in order. */
 lp_status lp_rig_set_streams(lp_rig* rig, int nstreams);
+/* Compositor launch chain replayed as a CUDA graph per frame slot (default
+ * 1); 0 launches every kernel individually. */
+lp_status lp_rig_set_graphs(lp_rig* rig, int on);
 
 #ifdef __cplusplus
 }

@@ -30,6 +30,10 @@ namespace lpb {
 
 static std::atomic<uint64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+// launches replayed inside a CUDA graph count as launches too
+static uint64_t launches_noted() { return g_launches.load(std::memory_order_relaxed); }
+static void note_launches(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
+static void unnote_launches(int n) { g_launches.fetch_sub(static_cast<uint64_t>(n), std::memory_order_relaxed); }
 static thread_local std::string g_err;
 
 // ---- kernel profiler: events around every launch, keyed "name/occurrence"
@@ -80,6 +84,7 @@ int prof_begin(const char* name, cudaStream_t s) {
     g_prof.open.push_back(r);
     return static_cast<int>(g_prof.open.size()) - 1;
 }
+static bool prof_active() { return g_prof.on; }
 void prof_end(int token, cudaStream_t s) {
     if (token < 0) return;
     std::lock_guard<std::mutex> l(g_prof.mu);

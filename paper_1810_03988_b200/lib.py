@@ -79,6 +79,8 @@ def load():
         lib.lp_rig_submit.restype = C.c_int
         lib.lp_rig_wait.argtypes = [P, C.c_uint64, C.POINTER(abi.Canvas)]
         lib.lp_rig_wait.restype = C.c_int
+        lib.lp_rig_set_graphs.argtypes = [P, C.c_int]
+        lib.lp_rig_set_graphs.restype = C.c_int
         lib.lp_rig_set_streams.argtypes = [P, C.c_int]
         lib.lp_rig_set_streams.restype = C.c_int
         lib.lp_rig_algorithmic_bytes.argtypes = [P, C.c_char_p]
@@ -188,6 +190,10 @@ class Rig:
             self.close()
         except Exception:
             pass
+
+    def set_graphs(self, on=True):
+        """Replay the compositor chain as a CUDA graph per frame slot (default on)."""
+        _check(self.lib, self.lib.lp_rig_set_graphs(self.rig, 1 if on else 0))
 
     def set_egress_rgb(self, on=True):
         """Panoramas leave the device as 3-channel RGB (the PPM sink's format)."""
