@@ -29,11 +29,27 @@
 namespace lpb {
 
 static std::atomic<uint64_t> g_launches{0};
-void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
-// launches replayed inside a CUDA graph count as launches too
-static uint64_t launches_noted() { return g_launches.load(std::memory_order_relaxed); }
+// launches recorded into a CUDA graph by this thread are counted when the
+// graph is replayed (note_launches), not at capture
+static thread_local bool t_capturing = false;
+void note_launch() {
+    if (!t_capturing) g_launches.fetch_add(1, std::memory_order_relaxed);
+}
 static void note_launches(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
-static void unnote_launches(int n) { g_launches.fetch_sub(static_cast<uint64_t>(n), std::memory_order_relaxed); }
+// kernel nodes of a captured graph
+static int graph_kernel_nodes(cudaGraph_t g) {
+    size_t n = 0;
+    LPB_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    if (n) LPB_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+    int k = 0;
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        LPB_CUDA(cudaGraphNodeGetType(nd, &t));
+        if (t == cudaGraphNodeTypeKernel) ++k;
+    }
+    return k;
+}
 static thread_local std::string g_err;
 
 // ---- kernel profiler: events around every launch, keyed "name/occurrence"
