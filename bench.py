@@ -456,7 +456,7 @@ def main():
 
     # ---- per-kernel profile pass (same workload; events around every launch)
     roofline = None
-    stage = {}
+    stage, stage_ms = {}, None
     if not args.no_profile:
         # per-kernel times are taken with the stages serialised (one stream) so
         # concurrent extraction does not inflate the compositor's kernels
@@ -504,8 +504,13 @@ def main():
                     "share_of_kernel_time": kern[dom][0] / max(1e-9, sum(v[0] for v in kern.values()))}
         stage = {k: round(v[0] / v[1], 4) for k, v in sorted(kern.items(), key=lambda kv: -kv[1][0])}
         stage["_kernel_ms_per_frame"] = round(step_ms, 4)
-        # frame-level HBM rate at SURVEY §8(d) algorithmic bytes per frame
-        stage["_per_frame_algorithmic_GBps"] = None
+        # the reference's stages (pipeline.hpp:26-34), device ms per frame
+        ref_stages = {"rectify_crop": ("k_rectify",), "detect": ("k_detect", "k_topn"),
+                      "describe": ("k_describe",),
+                      "match_estimate": ("k_lsh_keys", "k_match_query", "k_match_finalize", "k_prosac", "k_chain"),
+                      "warp_blend": ("k_warp", "k_runs", "k_mask0", "k_pyr_down", "k_blend_level")}
+        stage_ms = {name: round(sum(v[0] for k, v in kern.items() if k.split("/")[0] in ks) / args.steps, 4)
+                    for name, ks in ref_stages.items()}
 
     # ---- end to end through the public C-ABI with host buffers
     e2e = None
@@ -542,6 +547,26 @@ def main():
                          "host frames in and pinned host panoramas out",
                "last_panorama_sum": int(got)}
 
+    # frame-level HBM figure: SURVEY §8(d) compulsory bytes per frame (camera
+    # frames in, panorama out, the overlap strips' blur crops, keypoints and
+    # descriptors, and on re-registration frames the descriptors in and the
+    # matches + correspondences out) at the measured frame rate
+    frame_hbm = None
+    if rank == 0:
+        ov = 0.25
+        strip = int(np.floor(w * ov + 0.5))
+        ph, margin = 15, 21
+        crop_l = (min(w, w - ph + margin) - max(0, w - strip + ph - margin)) * h
+        crop_r = (min(w, strip - ph + margin) - max(0, ph - margin)) * h
+        nreg = 2 * (ncams - 1)
+        B = ncams * w * h + canvas[0] * canvas[1] + (ncams - 1) * (crop_l + crop_r) + nreg * 500 * 80
+        if cfgd["refresh"] == 1:
+            B += (ncams - 1) * (2 * 500 * 64 + 500 * 56)
+        gbps = B * value / 1e9
+        peak, peak_src = measured_peak_hbm()
+        frame_hbm = {"compulsory_bytes_per_frame": B, "GBps": gbps, "frac_of_peak": gbps / peak,
+                     "basis": "SURVEY 8(d) B_frame at the device frame rate"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         def params_fn(o):
@@ -561,7 +586,8 @@ def main():
                            "l2": f"{nsets} rotating input frame sets ({nsets * ncams * w * h / 1e6:.0f} MB) > 126 MB L2",
                            "parallelism": f"replicas x{world} (independent rigs, no data-path collective)"},
                 "gpu_launches": int(launches), "clocks": clk, "roofline": roofline,
-                "cpu_baseline": cpu, "e2e": e2e, "kernel_ms": stage, "rank_checksums": checksums}
+                "cpu_baseline": cpu, "e2e": e2e, "stage_ms": stage_ms if not args.no_profile else None,
+                "frame_hbm": frame_hbm, "kernel_ms": stage, "rank_checksums": checksums}
         s = json.dumps(line)
         print(s)
         if args.out:
