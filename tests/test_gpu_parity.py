@@ -431,3 +431,29 @@ def test_rig_graph_replay_matches_direct(lp, orc):
         a = direct.stitch([l, r], t)["panorama"]
         b = graph.stitch([l, r], t)["panorama"]
         assert np.array_equal(a, b), t
+
+
+def test_rig_nondefault_params_generic_paths(lp, orc):
+    """A 3-camera rig with non-default parameters: Harris sigma 1.5 and FAST
+    arc 10 (generic detect kernel), n_d 512 and blur sigma 3 (generic
+    describe), top_n 300, 6 blend levels (levels 5+ take the generic blend
+    kernel) and an odd frame size, bit-exact against the oracle."""
+    p = orc.default_params()
+    p.seed = p.matching.seed = 7
+    p.extraction.harris_sigma = 1.5
+    p.extraction.fast_arc = 10
+    p.extraction.n_d = 512
+    p.extraction.brief_blur_sigma = 3.0
+    p.extraction.top_n = 300
+    p.blend_levels = 6
+    cams, _, _ = chain_cameras(orc, 3, 501, 397, 0.25, 11)
+    got = lp.stitch_frame(cams, p, frame_index=0)
+    want = orc.stitch_frame(cams, p, frame_index=0)
+    assert got["canvas"] == want["canvas"]
+    for c in range(3):
+        assert np.array_equal(got["keypoints"][c], want["keypoints"][c]), c
+        assert np.array_equal(got["descriptors"][c], want["descriptors"][c]), c
+    for q in range(2):
+        assert np.array_equal(got["matches"][q], want["matches"][q]), q
+    assert np.array_equal(got["homographies"], want["homographies"])
+    assert np.array_equal(got["panorama"], want["panorama"])
