@@ -263,12 +263,14 @@ struct ExtractTables {
         for (size_t i = 0; i < 49; ++i) a.hw[i] = i < hw.size() ? hw[i] : 0.0;
         for (size_t i = 0; i < 2 * kMaxBlurR + 1; ++i) a.btaps[i] = i < tp.size() ? tp[i] : 0.0f;
     }
-    ExtractTables(const lp_extraction_config& c, const std::vector<lp_pair>& pat, cudaStream_t s) {
+    ExtractTables(const lp_extraction_config& c, const std::vector<lp_pair>& pat, cudaStream_t s,
+                  bool upload_now = true) {
         hw = host::harris_weights(c.harris_sigma, &harris_r);
         if (harris_r > kMaxHarrisR) throw Status(LP_BAD_PARAMS, "harris_sigma too large for the device tile");
         tp = host::gaussian_kernel(c.brief_blur_sigma);
         blur_r = static_cast<int>(tp.size() / 2);
         if (blur_r > kMaxBlurR) throw Status(LP_BAD_PARAMS, "brief_blur_sigma too large");
+        if (!upload_now) return;
         harris_w = upload(hw, s);
         taps = upload(tp, s);
         pairs = upload(pat, s);
@@ -319,6 +321,20 @@ struct lp_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // pinned staging for the one-shot calls (a ctx serves one thread at a time;
+    // every call leaves its stream idle, so growing it never races a copy)
+    void* pin = nullptr;
+    size_t pin_cap = 0;
+    uint8_t* staging(size_t bytes) {
+        if (bytes > pin_cap) {
+            if (pin) cudaFreeHost(pin);
+            pin = nullptr;
+            pin_cap = 0;
+            LPB_CUDA(cudaHostAlloc(&pin, std::max(bytes, size_t(1) << 20), cudaHostAllocDefault));
+            pin_cap = std::max(bytes, size_t(1) << 20);
+        }
+        return static_cast<uint8_t*>(pin);
+    }
 };
 
 extern "C" {
@@ -382,6 +398,12 @@ lp_status lp_ctx_create(int device, lp_ctx** out) {
             throw Status(LP_NO_DEVICE, "no CUDA device");
         }
         LPB_CUDA(cudaSetDevice(device));
+        // per-call scratch (cudaMallocAsync) stays cached in the device pool
+        // across synchronisations instead of going back to the driver each call
+        cudaMemPool_t pool;
+        LPB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = 1ull << 30;
+        LPB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         auto* c = new lp_ctx;
         c->device = device;
         LPB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -392,6 +414,7 @@ lp_status lp_ctx_create(int device, lp_ctx** out) {
 void lp_ctx_destroy(lp_ctx* ctx) {
     if (!ctx) return;
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->pin) cudaFreeHost(ctx->pin);
     delete ctx;
 }
 lp_status lp_ctx_set_stream(lp_ctx* ctx, void* s) {
@@ -599,28 +622,92 @@ lp_status lp_extract_features(lp_ctx* ctx, const uint8_t* img, int w, int h, int
         cudaStream_t s = ctx->stream;
         std::vector<lp_region> regs(regions, regions + nreg);
         std::vector<lp_pair> pat(pairs, pairs + cfg->n_d);
+        ExtractTables T(*cfg, pat, s, /*upload=*/false);
+        if (w > 65535 || h > 65535) throw Status(LP_BAD_PARAMS, "image dimension above 65535");
+        // A host image moves only its used rectangle: the regions plus the
+        // BRIEF crop margin (lorb.hpp:371-375) and the Harris window, packed
+        // into the call's pinned staging block. The extractor then runs on that
+        // sub-image with the regions shifted into it; every test it makes
+        // (segment ring, Harris window, patch fit, border clamps) lies inside
+        // the margin, or at a real image edge that the sub-image shares, so
+        // the results are those of the full image shifted back on the host.
+        const bool host_img = !is_device_ptr(img);
+        int bx0 = 0, by0 = 0, bw = w, bh = h;
+        if (host_img) {
+            const int M = std::max(cfg->patch_half + T.blur_r, T.harris_r + 2) + 4;
+            int x0 = w, y0 = h, x1 = 0, y1 = 0;
+            for (const auto& r : regs) {
+                x0 = std::min(x0, r.x0 - M);
+                y0 = std::min(y0, r.y0 - M);
+                x1 = std::max(x1, r.x1 + M);
+                y1 = std::max(y1, r.y1 + M);
+            }
+            x0 = std::max(x0, 0);
+            y0 = std::max(y0, 0);
+            x1 = std::min(x1, w);
+            y1 = std::min(y1, h);
+            if (x1 > x0 && y1 > y0) {
+                bx0 = x0;
+                by0 = y0;
+                bw = x1 - x0;
+                bh = y1 - y0;
+                for (auto& r : regs) {
+                    r.x0 -= bx0;
+                    r.x1 -= bx0;
+                    r.y0 -= by0;
+                    r.y1 -= by0;
+                }
+            }
+        }
         std::vector<int> zeros(nreg, 0);
         int tiles = 0;
-        auto dregs = make_dev_regions(regs, zeros, zeros, &w, &h, &tiles);
+        auto dregs = make_dev_regions(regs, zeros, zeros, &bw, &bh, &tiles);
         size_t scap = 0;
         for (auto& d : dregs) scap = std::max(scap, surv_cap_for(d));
-        ExtractTables T(*cfg, pat, s);
-        In<uint8_t> dimg(img, static_cast<size_t>(w) * h, s);
-        std::vector<DevImage> ims{DevImage{dimg.d, w, h}};
-        DBuf dims = upload(ims, s), dr = upload(dregs, s);
         const int W2 = 2 * ((cfg->n_d + 63) / 64);
         const int cap_slot = nreg * cfg->top_n;
+
+        // one staging block, mirrored in pinned host memory and on the device:
+        // inputs [image | DevImage | regions | tables | status] go up in one
+        // copy, outputs [status | count | keypoints | descriptors] come back in one
+        size_t off = 0;
+        auto put = [&](size_t bytes) {
+            const size_t o = off;
+            off = (off + bytes + 255) & ~size_t(255);
+            return o;
+        };
+        const size_t o_img = host_img ? put(static_cast<size_t>(bw) * bh) : 0;
+        const size_t o_dims = put(sizeof(DevImage)), o_regs = put(sizeof(DevRegion) * nreg),
+                     o_hw = put(sizeof(double) * T.hw.size()), o_tp = put(sizeof(float) * T.tp.size()),
+                     o_pairs = put(sizeof(lp_pair) * pat.size()), o_st = put(sizeof(int) * 2),
+                     o_kp = put(sizeof(lp_keypoint) * cap_slot),
+                     o_desc = put(sizeof(uint64_t) * static_cast<size_t>(cap_slot) * W2);
+        const size_t total_bytes = off;
+        uint8_t* hp = ctx->staging(total_bytes);
+        DBuf blk(total_bytes, s);
+        uint8_t* dp = blk.as<uint8_t>();
+        if (host_img)
+            for (int y = 0; y < bh; ++y)
+                std::memcpy(hp + o_img + static_cast<size_t>(y) * bw, img + static_cast<size_t>(y + by0) * w + bx0, bw);
+        const DevImage dim{host_img ? dp + o_img : img, bw, bh};
+        std::memcpy(hp + o_dims, &dim, sizeof dim);
+        std::memcpy(hp + o_regs, dregs.data(), sizeof(DevRegion) * nreg);
+        std::memcpy(hp + o_hw, T.hw.data(), sizeof(double) * T.hw.size());
+        std::memcpy(hp + o_tp, T.tp.data(), sizeof(float) * T.tp.size());
+        std::memcpy(hp + o_pairs, pat.data(), sizeof(lp_pair) * pat.size());
+        std::memset(hp + o_st, 0, sizeof(int) * 2);
+        LPB_CUDA(cudaMemcpyAsync(dp, hp, o_st + sizeof(int) * 2, cudaMemcpyHostToDevice, s));
+
         DBuf surv(sizeof(uint64_t) * scap * nreg, s), scount(sizeof(unsigned) * nreg, s),
             kpr(sizeof(lp_keypoint) * static_cast<size_t>(nreg) * cfg->top_n, s), cr(sizeof(int) * nreg, s),
-            kpo(sizeof(lp_keypoint) * cap_slot, s), dso(sizeof(uint64_t) * static_cast<size_t>(cap_slot) * W2, s),
-            sc(sizeof(int), s);
-        DevStatus st(s);
+            hist(sizeof(unsigned) * kTopnHistBins * nreg, s);
         ExtractArgs a{};
-        a.regions = dr.as<DevRegion>();
+        a.regions = reinterpret_cast<const DevRegion*>(dp + o_regs);
         a.nregions = nreg;
         a.max_tiles = tiles;
-        a.images = dims.as<DevImage>();
+        a.images = reinterpret_cast<const DevImage*>(dp + o_dims);
         T.fill(a);
+        a.harris_w = reinterpret_cast<const double*>(dp + o_hw);
         a.alpha = cfg->harris_alpha;
         a.threshold = cfg->harris_threshold;
         a.fast_t = static_cast<uint8_t>(cfg->fast_threshold);
@@ -628,34 +715,42 @@ lp_status lp_extract_features(lp_ctx* ctx, const uint8_t* img, int w, int h, int
         a.top_n = cfg->top_n;
         a.surv = surv.as<uint64_t>();
         a.surv_count = scount.as<unsigned>();
-        DBuf hist(sizeof(unsigned) * kTopnHistBins * nreg, s);
         a.hist = hist.as<unsigned>();
         a.surv_cap = static_cast<int>(scap);
         a.kp_region = kpr.as<lp_keypoint>();
         a.count_region = cr.as<int>();
-        a.blur_taps = T.taps.as<float>();
+        a.blur_taps = reinterpret_cast<const float*>(dp + o_tp);
         a.blur_r = T.blur_r;
-        a.pairs = T.pairs.as<lp_pair>();
+        a.pairs = reinterpret_cast<const lp_pair*>(dp + o_pairs);
         a.n_d = cfg->n_d;
         a.patch_half = cfg->patch_half;
         a.nslots = 1;
-        a.kp_out = kpo.as<lp_keypoint>();
-        a.desc_out = dso.as<uint64_t>();
+        a.kp_out = reinterpret_cast<lp_keypoint*>(dp + o_kp);
+        a.desc_out = reinterpret_cast<uint64_t*>(dp + o_desc);
         a.cap_slot = cap_slot;
-        a.slot_count = sc.as<int>();
-        a.status = st.ptr();
+        a.slot_count = reinterpret_cast<int*>(dp + o_st) + 1;
+        a.status = reinterpret_cast<int*>(dp + o_st);
         extract_launch(a, s);
-        sync_and_check(s, st.ptr());
-        int total = 0;
-        LPB_CUDA(cudaMemcpy(&total, sc.p, sizeof(int), cudaMemcpyDeviceToHost));
-        const int k = std::min(total, cap);
-        auto kind_k = is_device_ptr(kp_out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-        auto kind_d = is_device_ptr(desc_out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-        if (k > 0) {
-            LPB_CUDA(cudaMemcpyAsync(kp_out, kpo.p, sizeof(lp_keypoint) * k, kind_k, s));
-            LPB_CUDA(cudaMemcpyAsync(desc_out, dso.p, sizeof(uint64_t) * k * W2, kind_d, s));
-        }
+        LPB_CUDA(cudaMemcpyAsync(hp + o_st, dp + o_st, total_bytes - o_st, cudaMemcpyDeviceToHost, s));
         LPB_CUDA(cudaStreamSynchronize(s));
+        const int* hst = reinterpret_cast<const int*>(hp + o_st);
+        if (hst[0]) throw Status(static_cast<lp_status>(hst[0]), status_text(hst[0]));
+        const int total = hst[1];
+        const int k = std::min(total, cap);
+        auto* hk = reinterpret_cast<lp_keypoint*>(hp + o_kp);
+        for (int i = 0; i < k; ++i) {
+            hk[i].x += bx0;
+            hk[i].y += by0;
+        }
+        if (k > 0) {
+            const size_t kb = sizeof(lp_keypoint) * k, db = sizeof(uint64_t) * k * W2;
+            const bool dev_k = is_device_ptr(kp_out), dev_d = is_device_ptr(desc_out);
+            if (dev_k) LPB_CUDA(cudaMemcpyAsync(kp_out, hk, kb, cudaMemcpyHostToDevice, s));
+            else std::memcpy(kp_out, hk, kb);
+            if (dev_d) LPB_CUDA(cudaMemcpyAsync(desc_out, dp + o_desc, db, cudaMemcpyDeviceToDevice, s));
+            else std::memcpy(desc_out, hp + o_desc, db);
+            if (dev_k || dev_d) LPB_CUDA(cudaStreamSynchronize(s));
+        }
         *count = total;
     });
 }

@@ -47,9 +47,12 @@ def test_reference_unit_tests_on_b200_dropin(tmp_path):
 
 # The reference's acceptance suite (proj/tests/acceptance.cpp, 12 criteria,
 # unmodified). Criteria 8 and 9 are CPU-cost ratios (strip vs full-frame
-# extraction time, the thread pipeline's speedup over serial): on the GPU both
-# extractions are launch-bound (~0.2 ms each) and the stages are microseconds,
-# so those ratios do not describe the device path. Criterion 11 needs the CLI:
+# extraction time, the thread pipeline's speedup over serial). On the GPU a
+# host-image call moves only the used rectangle, so the strip costs 0.12 ms
+# against 0.19 ms for the full frame (ratio ~0.6, scripts/probes/
+# extract_timing.py): both describe the same top_n=500 keypoints and pay the
+# same launch + one-sync floor, so the 0.4 bound cannot hold; the stages are
+# microseconds, so criterion 9's thread speedup does not describe the device. Criterion 11 needs the CLI:
 # the B200 build drives this repo's CLI, the reference build has none (CLI11
 # absent here), and criterion 9 depends on the host's thread count.
 ACCEPT_B200_EXPECTED = {8, 9}
