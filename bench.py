@@ -411,7 +411,7 @@ def main():
     p = lp.default_params()
     p.seed = p.matching.seed = 42
     p.homography_refresh = cfgd["refresh"]
-    nsets = 8 if args.config in ("cfg3", "cfg4") else 4
+    nsets = int(os.environ.get("LPB_NSETS", 8 if args.config in ("cfg3", "cfg4") else 4))
     sets, shift = make_frame_sets(ncams, w, h, nsets, seed=42 + rank)
     dev_sets = [[torch.from_numpy(c).cuda() for c in s] for s in sets]
     rig = Rig(lp, ncams, w, h, p)
@@ -419,6 +419,8 @@ def main():
     pano_cap = rig.panorama_capacity()
     dpano = torch.empty(pano_cap, dtype=torch.uint8, device="cuda")
     fo = frame_out(dpano.data_ptr(), pano_cap)
+    dev_depth = int(os.environ.get("LPB_DEV_DEPTH", "1"))
+    dpanos = [dpano] + [torch.empty(pano_cap, dtype=torch.uint8, device="cuda") for _ in range(dev_depth - 1)]
 
     def step(i):
         rig.stitch_raw([t.data_ptr() for t in dev_sets[i % nsets]], i, fo)
@@ -439,8 +441,20 @@ def main():
     n0 = kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for i in range(args.steps):
-        step(args.warmup + i)
+    if dev_depth > 1:
+        # the rig's pipelined API (lp_rig_submit / lp_rig_wait), device-resident
+        # frames in and device panoramas out, dev_depth frames in flight
+        tickets = []
+        for i in range(args.steps):
+            tickets.append(rig.submit([t.data_ptr() for t in dev_sets[(args.warmup + i) % nsets]],
+                                      args.warmup + i, dpanos[i % dev_depth].data_ptr(), pano_cap))
+            if len(tickets) >= dev_depth:
+                rig.wait(tickets.pop(0))
+        for tk in tickets:
+            rig.wait(tk)
+    else:
+        for i in range(args.steps):
+            step(args.warmup + i)
     e1.record(stream)
     e1.synchronize()
     barrier()
@@ -449,7 +463,7 @@ def main():
     ms = e0.elapsed_time(e1)
     # the only collectives: MAX of device time, SUM of frames, gather of
     # panorama checksums (paper_1810_03988_b200.shard)
-    pano = dpano[:canvas[0] * canvas[1]]
+    pano = dpanos[(args.steps - 1) % dev_depth][:canvas[0] * canvas[1]] if dev_depth > 1 else dpano[:canvas[0] * canvas[1]]
     csum = int(pano.to(torch.int64).sum().item())
     ms_max, total_frames, checksums = gather_results(RankResult(args.steps, ms, csum), coll_dev)
     value = aggregate_fps(total_frames, ms_max)
@@ -525,7 +539,7 @@ def main():
         def run_e2e(n, base):
             tickets = []
             for i in range(n):
-                tickets.append(rig.submit([t.data_ptr() for t in host_sets[i % 2]], base + i,
+                tickets.append(rig.submit([t.data_ptr() for t in host_sets[i % len(host_sets)]], base + i,
                                           hpanos[i % depth].data_ptr(), pano_cap))
                 if len(tickets) >= depth:
                     rig.wait(tickets.pop(0))

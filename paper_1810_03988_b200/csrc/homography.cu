@@ -380,6 +380,37 @@ __device__ void block_dots(const double* v, int sv, const double* const* cols, i
     __syncthreads();
 }
 
+// phase timestamps of pair 0 (A/B builds only: scripts/variant.sh with
+// -DLPB_PROSAC_TRACE prints them from the device)
+#ifdef LPB_PROSAC_TRACE
+__device__ unsigned long long g_pt_t[64];
+__device__ const char* g_pt_tag[64];
+__device__ int g_pt_n;
+#define PTRACE(tag)                                                                          \
+    do {                                                                                     \
+        if (threadIdx.x == 0 && blockIdx.x == 0 && g_pt_n < 64) {                            \
+            unsigned long long t_;                                                           \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                           \
+            g_pt_t[g_pt_n] = t_;                                                             \
+            g_pt_tag[g_pt_n++] = tag;                                                        \
+        }                                                                                    \
+    } while (0)
+#define PTRACE_FLUSH()                                                                       \
+    do {                                                                                     \
+        if (threadIdx.x == 0 && blockIdx.x == 0) {                                          \
+            for (int i_ = 0; i_ < g_pt_n; ++i_) printf("PT %s %llu\n", g_pt_tag[i_], g_pt_t[i_]); \
+            g_pt_n = 0;                                                                      \
+        }                                                                                    \
+    } while (0)
+#else
+#define PTRACE(tag) \
+    do {            \
+    } while (0)
+#define PTRACE_FLUSH() \
+    do {               \
+    } while (0)
+#endif
+
 struct RefitShared {
     double red[9][256];
     double r[81];
@@ -426,6 +457,7 @@ __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, dou
         sh.nd = nd;
     }
     __syncthreads();
+    PTRACE("centroid");
     if (sh.status != LP_OK) return sh.status;
     {
         const Norm ns = sh.ns, nd = sh.nd;
@@ -449,6 +481,7 @@ __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, dou
         sh.nd.scale = md > 1e-12 ? sqrt(2.0) / md : 1.0;
     }
     __syncthreads();
+    PTRACE("scale");
     const Norm ns = sh.ns, nd = sh.nd;
     const int rows = 2 * m;
     for (int i = tid; i < m; i += blockDim.x) {
@@ -506,6 +539,7 @@ __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, dou
         }
     }
     __syncthreads();
+    PTRACE("qr");
     if (tid < 32) {
         double rr[9], hv[9];
 #pragma unroll
@@ -518,6 +552,7 @@ __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, dou
         }
     }
     __syncthreads();
+    PTRACE("svd");
     const int st = sh.status;
     for (int i = 0; i < 9; ++i) H[i] = sh.H[i];
     __syncthreads();
@@ -571,6 +606,7 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
     const int pair = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (a.pair_status[pair] != LP_OK) return;
+    PTRACE("start");
     const int n = a.counts[pair];
     const lp_corr* m = a.corr + static_cast<size_t>(pair) * a.cap;
     if (n < 4) {
@@ -626,11 +662,13 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
             }
         }
         __syncthreads();
+        PTRACE("sampled");
         if (warp < chunk) {
             lp_corr q[4];
             for (int i = 0; i < 4; ++i) q[i] = m[S.samples[warp][i]];
             double H[9], Hi[9];
             const bool ok = dlt_minimal_warp(q, H) == LP_OK && h_inverse(H, Hi);
+            PTRACE("minimal");
             if (ok) {
                 int count = 0;
                 double err = 0.0;
@@ -664,6 +702,7 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
             if (lane == 0) S.valid[warp] = ok;
         }
         __syncthreads();
+        PTRACE("scored");
         if (tid == 0) {
             for (int h = 0; h < chunk; ++h) {
                 const int t = t0 + h;
@@ -713,6 +752,7 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
     const int n_in = block_compact(n, idx, [&](int i) { return ste(bh, bhi, m[i]) <= a.threshold; });
     double Hr[9], Hri[9];
     int st;
+    PTRACE("compacted");
     if (n_in <= a.smem_rows) {
         // the inliers and the whole refit system in shared memory: the
         // sequential Hartley sums and the blocked QR passes read on-chip
@@ -723,6 +763,7 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
         lp_corr* sc = reinterpret_cast<lp_corr*>(st_terms + 2 * a.smem_rows);
         for (int i = tid; i < n_in; i += blockDim.x) sc[i] = m[idx[i]];
         __syncthreads();
+        PTRACE("staged");
         st = dlt_block(sc, nullptr, n_in, sA, sv, st_terms, Hr, S.refit);
     } else {
         st = dlt_block(m, idx, n_in, A, vbuf, terms, Hr, S.refit);
@@ -750,6 +791,8 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
     for (int off = 16; off > 0; off >>= 1) local += __shfl_xor_sync(kFull, local, off);
     if (lane == 0) atomicAdd(&S.final_count, local);
     __syncthreads();
+    PTRACE("end");
+    PTRACE_FLUSH();
     if (tid == 0) {
         const int cnt = S.final_count;
         for (int i = 0; i < 9; ++i) a.model[pair].h[i] = fh[i];
