@@ -737,23 +737,24 @@ static void svd_null_vector(double* a, int m, double* hv) {
     double r[N * N];
     memset(r, 0, sizeof r);
     if (m > N) {
-        double* v = xcalloc((size_t)m, sizeof(double));
+        /* Householder step j, sums below the diagonal in the canonical
+         * blocked order, diagonal terms separately (shim) */
         for (int j = 0; j < N; ++j) {
-            const double normx = sqrt(dot_blocked(a + j, N, a + j, N, j, m));
-            if (normx == 0.0) continue;
+            const double S = dot_blocked(a + j, N, a + j, N, j + 1, m);
             const double alpha = a[(size_t)j * N + j];
+            const double normx = sqrt(alpha * alpha + S);
+            if (normx == 0.0) continue;
             const double beta = alpha >= 0.0 ? -normx : normx;
-            for (int i = 0; i < m; ++i) v[i] = i < j ? 0.0 : a[(size_t)i * N + j];
-            v[j] = alpha - beta;
-            const double vn2 = dot_blocked(v, 1, v, 1, j, m);
+            const double v0 = alpha - beta;
+            const double vn2 = v0 * v0 + S;
             for (int k = j + 1; k < N; ++k) {
-                const double f = 2.0 * dot_blocked(v, 1, a + k, N, j, m) / vn2;
-                for (int i = j; i < m; ++i) a[(size_t)i * N + k] = a[(size_t)i * N + k] - f * v[i];
+                const double f = 2.0 * (v0 * a[(size_t)j * N + k] + dot_blocked(a + j, N, a + k, N, j + 1, m)) / vn2;
+                a[(size_t)j * N + k] = a[(size_t)j * N + k] - f * v0;
+                for (int i = j + 1; i < m; ++i) a[(size_t)i * N + k] = a[(size_t)i * N + k] - f * a[(size_t)i * N + j];
             }
             a[(size_t)j * N + j] = beta;
             for (int i = j + 1; i < m; ++i) a[(size_t)i * N + j] = 0.0;
         }
-        free(v);
         for (int i = 0; i < N; ++i)
             for (int k = 0; k < N; ++k) r[i * N + k] = k < i ? 0.0 : a[(size_t)i * N + k];
     } else {
@@ -779,10 +780,12 @@ static void svd_null_vector(double* a, int m, double* hv) {
                 if (ga == 0.0 || ga * ga <= eps2 * (al * be) || fabs(ga) <= 2.220446049250313e-16 * fmax(al, be))
                     continue;
                 rotated = 1;
-                const double zeta = (be - al) / (2.0 * ga);
-                const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                const double c = 1.0 / sqrt(1.0 + t * t);
-                const double s = c * t;
+                /* tan = sgn(d) 2g / (|d| + hypot(d, 2g)), d = be - al (shim) */
+                const double d = be - al, g2 = 2.0 * ga;
+                const double u = fabs(d) + sqrt(d * d + g2 * g2);
+                const double w = sqrt(u * u + g2 * g2);
+                const double c = u / w;
+                const double s = (d >= 0.0 ? g2 : -g2) / w;
                 for (int i = 0; i < N; ++i) {
                     const double up = r[i * N + p], uq = r[i * N + q];
                     r[i * N + p] = c * up - s * uq;

@@ -146,79 +146,82 @@ struct Norm {
 // ---- warp-parallel one-sided Jacobi SVD of a 9x9 factor ----
 constexpr unsigned kFull = 0xffffffffu;
 
-// sum of v over lanes 0..8 in the order (((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)))+p8
-// (oracle/shim/Eigen/Dense dot9); result broadcast to every lane
-__device__ __forceinline__ double tree9(double v) {
-    const double t = v + __shfl_down_sync(kFull, v, 1);
-    const double u = t + __shfl_down_sync(kFull, t, 2);
-    const double w = u + __shfl_down_sync(kFull, u, 4);
-    const double s = w + __shfl_sync(kFull, v, 8);
-    return __shfl_sync(kFull, s, 0);
+
+// dot9's fixed pairwise order (oracle/shim/Eigen/Dense) over one lane's
+// column: (((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)))+p8
+__device__ __forceinline__ double col_dot9(const double (&a)[9], const double (&b)[9]) {
+    double p[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) p[i] = a[i] * b[i];
+    return (((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]))) + p[8];
 }
 
-// Lane i (< 9) holds row i of the factor in rr; lanes >= 9 hold zeros. On
-// return every lane holds the whole null vector hv (V column of the smallest
-// singular value, stable descending order as Eigen::JacobiSVD sorts).
-__device__ void warp_jacobi_null(double (&rr)[9], double (&hv)[9]) {
+// Lane j (< 9) holds column j of the 9x9 factor in col (col[i] = R(i, j));
+// lanes >= 9 hold zeros. On return every lane holds the whole null vector hv
+// (V column of the smallest singular value, stable descending order as
+// Eigen::JacobiSVD sorts).
+//
+// Round-robin ordering shared with the oracles: round r rotates the four
+// disjoint column pairs {(r+k) mod 9, (r-k) mod 9}, k = 1..4, i.e. lane j's
+// partner is (2r - j) mod 9 (lane r mod 9 rests). Both lanes of a pair fetch
+// each other's R and V columns (18 shuffles for all four pairs), form alpha,
+// beta, gamma locally in dot9's order, compute the same rotation and update
+// their own column: the products, sums and rotation formulas of the oracle,
+// so the result is bit-identical to it.
+__device__ void warp_jacobi_null(double (&col)[9], double (&hv)[9]) {
     const int lane = threadIdx.x & 31;
     double V[9];
 #pragma unroll
-    for (int j = 0; j < 9; ++j) V[j] = lane == j ? 1.0 : 0.0;
+    for (int i = 0; i < 9; ++i) V[i] = lane == i ? 1.0 : 0.0;
     const double eps2 = 1e-30;
     for (int sweep = 0; sweep < 60; ++sweep) {
         bool rotated = false;
-        // round-robin ordering shared with the oracles: round r rotates the
-        // four disjoint pairs {(r+k) mod 9, (r-k) mod 9}, k = 1..4, which
-        // commute exactly, so their 12 dot products and 4 rotations overlap
-#pragma unroll
+#pragma unroll 1
         for (int rnd = 0; rnd < 9; ++rnd) {
-            double al[4], be[4], ga[4];
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-                const int a0 = (rnd + kk + 1) % 9, b0 = (rnd - kk - 1 + 9) % 9;
-                const int p = a0 < b0 ? a0 : b0, q = a0 < b0 ? b0 : a0;
-                al[kk] = tree9(rr[p] * rr[p]);
-                be[kk] = tree9(rr[q] * rr[q]);
-                ga[kk] = tree9(rr[p] * rr[q]);
+            int partner = lane;
+            if (lane < 9) {
+                partner = 2 * rnd - lane;
+                partner += partner < 0 ? 9 : 0;
+                partner += partner < 0 ? 9 : 0;
+                partner -= partner >= 9 ? 9 : 0;
             }
-            // the four rotations' scalar work (divisions, square roots) runs
-            // once, on lanes 0..3 in parallel, instead of four times in series
-            // on every lane; (c, s) are then broadcast. Same formulas, same
-            // rounding: lane kk computes exactly what every lane computed.
-            const int kr = lane & 3;
-            const double alk = kr == 0 ? al[0] : kr == 1 ? al[1] : kr == 2 ? al[2] : al[3];
-            const double bek = kr == 0 ? be[0] : kr == 1 ? be[1] : kr == 2 ? be[2] : be[3];
-            const double gak = kr == 0 ? ga[0] : kr == 1 ? ga[1] : kr == 2 ? ga[2] : ga[3];
-            const bool skip = gak == 0.0 || gak * gak <= eps2 * (alk * bek) ||
-                              fabs(gak) <= 2.220446049250313e-16 * fmax(alk, bek);
-            double ck = 1.0, sk = 0.0;
-            if (!skip) {
-                const double zeta = (bek - alk) / (2.0 * gak);
-                const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                ck = 1.0 / sqrt(1.0 + t * t);
-                sk = ck * t;
-            }
-            const unsigned rot = __ballot_sync(kFull, !skip) & 0xFu;
-            if (rot) rotated = true;
+            double oc[9], ov[9];
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-                const int a0 = (rnd + kk + 1) % 9, b0 = (rnd - kk - 1 + 9) % 9;
-                const int p = a0 < b0 ? a0 : b0, q = a0 < b0 ? b0 : a0;
-                const double c = __shfl_sync(kFull, ck, kk), s = __shfl_sync(kFull, sk, kk);
-                if (!((rot >> kk) & 1u)) continue;
-                const double up = rr[p], uq = rr[q];
-                rr[p] = c * up - s * uq;
-                rr[q] = s * up + c * uq;
-                const double vp = V[p], vq = V[q];
-                V[p] = c * vp - s * vq;
-                V[q] = s * vp + c * vq;
+            for (int i = 0; i < 9; ++i) oc[i] = __shfl_sync(kFull, col[i], partner);
+#pragma unroll
+            for (int i = 0; i < 9; ++i) ov[i] = __shfl_sync(kFull, V[i], partner);
+            if (partner == lane) continue;
+            const bool low = lane < partner;  // this lane holds column p (p < q)
+            const double own = col_dot9(col, col), other = col_dot9(oc, oc), ga = col_dot9(col, oc);
+            const double al = low ? own : other, be = low ? other : own;
+            if (ga == 0.0 || ga * ga <= eps2 * (al * be) || fabs(ga) <= 2.220446049250313e-16 * fmax(al, be))
+                continue;
+            rotated = true;
+            // the rotation that zeroes gamma: tan = sgn(d) 2g / (|d| + hypot(d, 2g)),
+            // d = beta - alpha, as c = u / w and s = sgn(d) 2g / w with
+            // u = |d| + hypot(d, 2g), w = hypot(u, 2g): two square roots and
+            // two independent divisions on the dependency chain
+            const double d = be - al, g2 = 2.0 * ga;
+            const double u = fabs(d) + sqrt(d * d + g2 * g2);
+            const double w = sqrt(u * u + g2 * g2);
+            const double c = u / w;
+            const double sn = (d >= 0.0 ? g2 : -g2) / w;
+            // column p: c*up - s*uq; column q: s*up + c*uq. Both as
+            // c*own + s'*other with s' = -s on p (negation and commuted
+            // addition are exact), so the pair runs without divergence
+            const double so = low ? -sn : sn;
+#pragma unroll
+            for (int i = 0; i < 9; ++i) {
+                col[i] = c * col[i] + so * oc[i];
+                V[i] = c * V[i] + so * ov[i];
             }
         }
-        if (!rotated) break;
+        if (!__any_sync(kFull, rotated)) break;
     }
+    const double myv = sqrt(col_dot9(col, col));
     double sv[9];
 #pragma unroll
-    for (int j = 0; j < 9; ++j) sv[j] = sqrt(tree9(rr[j] * rr[j]));
+    for (int j = 0; j < 9; ++j) sv[j] = __shfl_sync(kFull, myv, j);
     int order[9];
 #pragma unroll
     for (int i = 0; i < 9; ++i) order[i] = i;
@@ -232,12 +235,8 @@ __device__ void warp_jacobi_null(double (&rr)[9], double (&hv)[9]) {
         order[j + 1] = x;
     }
     const int jmin = order[8];
-    double mine = 0.0;
 #pragma unroll
-    for (int j = 0; j < 9; ++j)
-        if (j == jmin) mine = V[j];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) hv[i] = __shfl_sync(kFull, mine, i);
+    for (int i = 0; i < 9; ++i) hv[i] = __shfl_sync(kFull, V[i], jmin);
 }
 
 // denormalise H = Td^-1 * Hn * Ts, scale h33, degeneracy checks
@@ -314,74 +313,40 @@ __device__ int dlt_minimal_warp(const lp_corr* p, double* H) {
     md /= 4.0;
     ns.scale = ms > 1e-12 ? sqrt(2.0) / ms : 1.0;
     nd.scale = md > 1e-12 ? sqrt(2.0) / md : 1.0;
-    double rr[9];
+    // column `lane` of the 8x9 system (zero-padded to 9x9): rows 2k, 2k+1 of
+    // point k are [-x,-y,-1,0,0,0,ux,uy,u] and [0,0,0,-x,-y,-1,vx,vy,v]
+    double cl[9];
 #pragma unroll
-    for (int j = 0; j < 9; ++j) rr[j] = 0.0;
-    if (lane < 8) {  // row `lane` of the 8x9 system (zero-padded to 9x9)
-        const lp_corr c = p[lane >> 1];
+    for (int i = 0; i < 9; ++i) cl[i] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const lp_corr c = p[k];
         const double x = (c.sx - ns.cx) * ns.scale, y = (c.sy - ns.cy) * ns.scale;
         const double u = (c.dx - nd.cx) * nd.scale, v = (c.dy - nd.cy) * nd.scale;
-        if ((lane & 1) == 0) {
-            rr[0] = -x; rr[1] = -y; rr[2] = -1; rr[6] = u * x; rr[7] = u * y; rr[8] = u;
-        } else {
-            rr[3] = -x; rr[4] = -y; rr[5] = -1; rr[6] = v * x; rr[7] = v * y; rr[8] = v;
+        double e0 = 0.0, e1 = 0.0;
+        switch (lane) {
+            case 0: e0 = -x; break;
+            case 1: e0 = -y; break;
+            case 2: e0 = -1; break;
+            case 3: e1 = -x; break;
+            case 4: e1 = -y; break;
+            case 5: e1 = -1; break;
+            case 6: e0 = u * x; e1 = v * x; break;
+            case 7: e0 = u * y; e1 = v * y; break;
+            case 8: e0 = u; e1 = v; break;
+            default: break;
         }
+        cl[2 * k] = e0;
+        cl[2 * k + 1] = e1;
     }
     double hv[9];
-    warp_jacobi_null(rr, hv);
+    warp_jacobi_null(cl, hv);
     return dlt_denormalize(hv, ns, nd, H);
 }
 
 // ---- block-wide pieces (blockDim.x == 256) ----
-// canonical blocked dot products (oracle/shim/Eigen/Dense dot_blocked): lane
-// l = row & 255 accumulates rows in increasing order, then the pairwise tree
-// p[l] += p[l+s], s = 128..1 (s >= 32 in shared memory, s <= 16 by shuffles)
-// SELF: column 0 is v itself (v.v beside the v.col_k, one pass, each in the
-// same canonical order as its own call)
-template <int K, bool SELF = false>
-__device__ void block_dots(const double* v, int sv, const double* const* cols, int sc, int r0,
-                           int r1, double (*s_red)[256], double* out) {
-    const int l = threadIdx.x;
-    double p[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) p[k] = 0.0;
-    const int i0 = r0 + ((l - (r0 & 255)) & 255);
-    for (int i = i0; i < r1; i += 256) {
-        const double vi = v[static_cast<size_t>(i) * sv];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            if (SELF && k == 0)
-                p[0] = p[0] + vi * vi;
-            else if (cols[k])
-                p[k] = p[k] + vi * cols[k][static_cast<size_t>(i) * sc];
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) s_red[k][l] = p[k];
-    __syncthreads();
-    // the canonical tree p[l] += p[l + s], s = 128, 64, 32, then shuffles
-    // 16..1, all in warp 0 (lane l owns partial sums l, l+32, l+64, l+96):
-    // the same additions in the same order with one barrier instead of four
-    if (l < 32) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const double a0 = s_red[k][l] + s_red[k][l + 128];
-            const double a1 = s_red[k][l + 32] + s_red[k][l + 160];
-            const double a2 = s_red[k][l + 64] + s_red[k][l + 192];
-            const double a3 = s_red[k][l + 96] + s_red[k][l + 224];
-            double x = (a0 + a2) + (a1 + a3);
-            for (int s = 16; s >= 1; s >>= 1) x = x + __shfl_down_sync(kFull, x, s);
-            if (l == 0) s_red[k][0] = x;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < K; ++k) out[k] = s_red[k][0];
-    __syncthreads();
-}
-
 // phase timestamps of pair 0 (A/B builds only: scripts/variant.sh with
-// -DLPB_PROSAC_TRACE prints them from the device)
+// -DLPB_PROSAC_TRACE; scripts/probes/prosac_trace.py prints them)
 #ifdef LPB_PROSAC_TRACE
 __device__ unsigned long long g_pt_t[64];
 __device__ const char* g_pt_tag[64];
@@ -415,6 +380,8 @@ struct RefitShared {
     double red[9][256];
     double r[81];
     double H[9];
+    double f[8], beta, v0;  // one Householder step's scalars
+    int skip;
     Norm ns, nd;
     int status;
 };
@@ -497,37 +464,75 @@ __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, dou
     }
     __syncthreads();
     if (rows > 9) {
-        // Householder QR (oracle/shim/Eigen/Dense JacobiSVD preconditioner)
+        // Householder QR (oracle/shim/Eigen/Dense JacobiSVD preconditioner).
+        // Step j needs S = sum_{i>j} a_ij^2 and D_k = sum_{i>j} a_ij a_ik in
+        // the canonical blocked order (lane = row & 255, rows ascending, then
+        // the pairwise tree): thread t owns rows i = t mod 256 throughout, so
+        // the pass that applies step j also accumulates step j+1's partial
+        // sums from the rows it just wrote; one block reduction per column.
+        double pp[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) pp[k] = 0.0;
+        auto acc = [&](const double* row, int jj) {
+            const double x = row[jj];
+            pp[0] = pp[0] + x * x;
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                if (jj + 1 + t < 9) pp[1 + t] = pp[1 + t] + x * row[jj + 1 + t];
+        };
+        for (int i = tid; i < rows; i += 256)
+            if (i > 0) acc(A + static_cast<size_t>(i) * 9, 0);
         for (int j = 0; j < 9; ++j) {
-            const double* cj[1] = {A + j};
-            double nrm2;
-            block_dots<1>(A + j, 9, cj, 9, j, rows, sh.red, &nrm2);
-            const double normx = sqrt(nrm2);
-            if (normx == 0.0) continue;
-            const double alpha = A[static_cast<size_t>(j) * 9 + j];
-            const double beta = alpha >= 0.0 ? -normx : normx;
-            for (int i = tid; i < rows; i += blockDim.x)
-                vbuf[i] = i < j ? 0.0 : (i == j ? alpha - beta : A[static_cast<size_t>(i) * 9 + j]);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) sh.red[k][tid] = pp[k];
             __syncthreads();
-            // v.v and v.A_k (k > j) in one pass
-            const double* ck[9];
-            ck[0] = vbuf;
-            for (int k = 0; k < 8; ++k) ck[k + 1] = (j + 1 + k < 9) ? A + j + 1 + k : nullptr;
-            double vd[9];
-            block_dots<9, true>(vbuf, 1, ck, 9, j, rows, sh.red, vd);
-            const double vn2 = vd[0];
-            double dk[8];
-            for (int k = 0; k < 8; ++k) dk[k] = vd[k + 1];
-            double f[8];
-            for (int k = 0; k < 8; ++k) f[k] = 2.0 * dk[k] / vn2;
-            for (int i = j + tid; i < rows; i += blockDim.x) {
-                const double vi = vbuf[i];
-                double* row = A + static_cast<size_t>(i) * 9;
-                for (int k = j + 1; k < 9; ++k) row[k] = row[k] - f[k - j - 1] * vi;
-                row[j] = i == j ? beta : 0.0;
+            if (tid < 32) {
+                double red[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    const double a0 = sh.red[k][tid] + sh.red[k][tid + 128];
+                    const double a1 = sh.red[k][tid + 32] + sh.red[k][tid + 160];
+                    const double a2 = sh.red[k][tid + 64] + sh.red[k][tid + 192];
+                    const double a3 = sh.red[k][tid + 96] + sh.red[k][tid + 224];
+                    double x = (a0 + a2) + (a1 + a3);
+                    for (int o = 16; o >= 1; o >>= 1) x = x + __shfl_down_sync(kFull, x, o);
+                    red[k] = x;
+                }
+                if (tid == 0) {
+                    const double* rj = A + static_cast<size_t>(j) * 9;
+                    const double alpha = rj[j];
+                    const double normx = sqrt(alpha * alpha + red[0]);
+                    sh.skip = normx == 0.0;
+                    const double beta = alpha >= 0.0 ? -normx : normx;
+                    const double v0 = alpha - beta;
+                    const double vn2 = v0 * v0 + red[0];
+                    for (int t = 0; t < 8; ++t)
+                        sh.f[t] = j + 1 + t < 9 ? 2.0 * (v0 * rj[j + 1 + t] + red[1 + t]) / vn2 : 0.0;
+                    sh.beta = beta;
+                    sh.v0 = v0;
+                }
             }
             __syncthreads();
+            const bool skip = sh.skip;
+            double f[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) f[t] = sh.f[t];
+            const double beta = sh.beta, v0 = sh.v0;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) pp[k] = 0.0;
+            for (int i = j + ((tid - j) & 255); i < rows; i += 256) {
+                double* row = A + static_cast<size_t>(i) * 9;
+                if (!skip) {
+                    const double vi = i == j ? v0 : row[j];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        if (j + 1 + t < 9) row[j + 1 + t] = row[j + 1 + t] - f[t] * vi;
+                    row[j] = i == j ? beta : 0.0;
+                }
+                if (j < 8 && i > j + 1) acc(row, j + 1);
+            }
         }
+        __syncthreads();
         for (int i = tid; i < 81; i += blockDim.x) {
             const int r = i / 9, c = i % 9;
             sh.r[i] = c < r ? 0.0 : A[static_cast<size_t>(r) * 9 + c];
@@ -541,10 +546,10 @@ __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, dou
     __syncthreads();
     PTRACE("qr");
     if (tid < 32) {
-        double rr[9], hv[9];
+        double cl[9], hv[9];
 #pragma unroll
-        for (int j = 0; j < 9; ++j) rr[j] = tid < 9 ? sh.r[tid * 9 + j] : 0.0;
-        warp_jacobi_null(rr, hv);
+        for (int i = 0; i < 9; ++i) cl[i] = tid < 9 ? sh.r[i * 9 + tid] : 0.0;
+        warp_jacobi_null(cl, hv);
         if (tid == 0) {
             double Hh[9];
             sh.status = dlt_denormalize(hv, ns, nd, Hh);

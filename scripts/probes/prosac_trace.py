@@ -4,6 +4,8 @@ sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
 if len(sys.argv) < 2:
     out = subprocess.run([sys.executable, __file__, "run"], capture_output=True, text=True).stdout
     rows = [l.split() for l in out.splitlines() if l.startswith("PT ")]
+    sw = [l.split()[1] for l in out.splitlines() if l.startswith("PT-sweeps")]
+    print("jacobi sweeps (block 0, warp 0):", " ".join(sw[-8:]))
     frames, cur = [], []
     for _, tag, t in rows:
         if tag == "start" and cur:
