@@ -186,13 +186,17 @@ __device__ void warp_jacobi_null(double (&col)[9], double (&hv)[9]) {
                 partner -= partner >= 9 ? 9 : 0;
             }
             double oc[9], ov[9];
+            // each lane's own squared norm is its partner's other one (the
+            // same products in the same order): one shuffle instead of a dot
+            const double own = col_dot9(col, col);
+            const double other = __shfl_sync(kFull, own, partner);
 #pragma unroll
             for (int i = 0; i < 9; ++i) oc[i] = __shfl_sync(kFull, col[i], partner);
 #pragma unroll
             for (int i = 0; i < 9; ++i) ov[i] = __shfl_sync(kFull, V[i], partner);
             if (partner == lane) continue;
             const bool low = lane < partner;  // this lane holds column p (p < q)
-            const double own = col_dot9(col, col), other = col_dot9(oc, oc), ga = col_dot9(col, oc);
+            const double ga = col_dot9(col, oc);
             const double al = low ? own : other, be = low ? other : own;
             if (ga == 0.0 || ga * ga <= eps2 * (al * be) || fabs(ga) <= 2.220446049250313e-16 * fmax(al, be))
                 continue;
@@ -630,6 +634,7 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
                                   ? (a.seed ^ (a.frame * 0x9e3779b97f4a7c15ull + static_cast<uint64_t>(pair)))
                                   : a.seed;
         mt_seed(S.rng, seed);
+        PTRACE("seeded");
         t_n = a.t_total;
         for (int i = 0; i < 4; ++i) t_n *= static_cast<double>(4 - i) / (n - i);
         pool = a.uniform ? n : 4;
@@ -641,6 +646,7 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
     __syncthreads();
     if (warp == 0) mt_twist_warp(S.rng);  // the first draw's twist, in parallel
     __syncthreads();
+    PTRACE("twisted");
     const int* exit_row = a.exit_tab + (a.nmax > 0 ? static_cast<size_t>(n) * (a.nmax + 1) : 0);
     for (int t0 = 1; t0 <= a.max_iter; t0 += kChunk) {
         const int chunk = min(kChunk, a.max_iter - t0 + 1);
