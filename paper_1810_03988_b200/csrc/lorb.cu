@@ -275,10 +275,13 @@ __global__ void __launch_bounds__(256, 4) k_detect9(const __grid_constant__ Extr
     if (inside) {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(im.p + static_cast<size_t>(gy0) * im.w + gx0);
         const int pitch = im.w >> 2;
+        // register-free global->shared copies: every word of the tile in
+        // flight at once instead of a load->store latency per iteration
         for (int i = tid; i < SH * SWW; i += 256) {
             const int r = i / SWW, q = i - r * SWW;
-            s_img[i] = __ldg(src + static_cast<size_t>(r) * pitch + q);
+            cp_async4(&s_img[i], src + static_cast<size_t>(r) * pitch + q, true);
         }
+        cp_async_wait_all();
     } else {  // clamped bytes; clamped texels never reach a valid test
         for (int i = tid; i < SH * SWW; i += 256) {
             const int r = i / SWW, q = i - r * SWW;

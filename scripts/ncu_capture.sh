@@ -5,7 +5,7 @@ cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 CFG=${CFG:-cfg3}
 TAG=${TAG:-cap}
-timeout ${NCU_TIMEOUT:-900} ncu --set full --clock-control none --import-source on ${NCU_EXTRA} \
+LPB_GRAPHS=0 timeout ${NCU_TIMEOUT:-900} ncu --set full --clock-control none --import-source on ${NCU_EXTRA} \
     -k regex:"${KREGEX:-k_detect}" -s ${KSKIP:-4} -c ${KCOUNT:-4} \
     -o gpurun_out/$TAG -f python bench.py --config $CFG --steps ${STEPS:-3} --warmup 1 --no-e2e \
     --no-cpu-baseline --no-profile > gpurun_out/${TAG}_run.log 2>&1
