@@ -13,6 +13,8 @@ tail -3 gpurun_out/${TAG}_run.log
 ncu -i gpurun_out/$TAG.ncu-rep --page raw --csv > gpurun_out/${TAG}_raw.csv 2>/dev/null
 # per-instruction source pages of the captured launches (stall sampling)
 ncu -i gpurun_out/$TAG.ncu-rep --page source --csv --print-source sass > gpurun_out/${TAG}_sass.csv 2>/dev/null
+# and per CUDA source line (-lineinfo build)
+ncu -i gpurun_out/$TAG.ncu-rep --page source --csv --print-source cuda > gpurun_out/${TAG}_cuda.csv 2>/dev/null
 # the full report only when asked (gpurun brings back <= 64 MiB)
 [ "${KEEP_REP:-0}" = "1" ] || rm -f gpurun_out/$TAG.ncu-rep
 ls -la gpurun_out
