@@ -15,21 +15,37 @@
 
 namespace lpb {
 
+// one warp per descriptor: lane b extracts bit b of a table's key (hash_key,
+// matchlsh.hpp:70-80) and a ballot assembles the key; all tables' loads are
+// issued before the ballots
 __global__ void k_lsh_keys(MatchArgs a) {
-    const int gi = blockIdx.x * blockDim.x + threadIdx.x;
-    const int slot = gi / a.cap, i = gi - slot * a.cap;
-    if (slot >= a.nslots || i >= a.counts[slot]) return;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int slot = gw / a.cap, i = gw - slot * a.cap;
+    if (slot >= a.nslots || i >= a.counts[slot]) return;  // warp-uniform
     const int W = (a.n_d + 63) / 64;
     const uint64_t* d = a.desc + (static_cast<size_t>(slot) * a.cap + i) * 2 * W;
-    for (int t = 0; t < a.tables; ++t) {
-        uint64_t key = 0;
-        for (int b = 0; b < a.bits; ++b) {
-            const int p = a.bitpos[t * a.bits + b];
-            const uint64_t* plane = p < a.n_d ? d : d + W;
-            const int bit = p < a.n_d ? p : p - a.n_d;
-            key |= ((plane[bit >> 6] >> (bit & 63)) & 1ull) << b;
+    uint64_t* out = a.keys + (static_cast<size_t>(slot) * a.cap + i) * a.tables;
+    for (int t0 = 0; t0 < a.tables; t0 += 4) {
+        unsigned bits[4][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int t = t0 + u, b = 32 * h + lane;
+                unsigned v = 0;
+                if (t < a.tables && b < a.bits) {
+                    const int p = __ldg(a.bitpos + t * a.bits + b);
+                    const int q = p < a.n_d ? p : p - a.n_d;  // bit within its plane
+                    v = static_cast<unsigned>((__ldg(d + (p < a.n_d ? 0 : W) + (q >> 6)) >> (q & 63)) & 1ull);
+                }
+                bits[u][h] = v;
+            }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint64_t lo = __ballot_sync(0xffffffffu, bits[u][0]);
+            const uint64_t hi = __ballot_sync(0xffffffffu, bits[u][1]);
+            if (lane == 0 && t0 + u < a.tables) out[t0 + u] = lo | (hi << 32);
         }
-        a.keys[(static_cast<size_t>(slot) * a.cap + i) * a.tables + t] = key;
     }
 }
 
@@ -55,10 +71,11 @@ __device__ __forceinline__ void top2_insert(int d, int j, int& d0, int& j0, int&
     }
 }
 
-constexpr int kQueriesPerWarp = 1;
 constexpr int kMaxW = 8;  // n_d <= 512
 
-__global__ void __launch_bounds__(256) k_match_query(MatchArgs a) {
+// one warp per query (large problems: enough warps, and a small register
+// footprint keeps 6 CTAs per SM resident)
+__global__ void __launch_bounds__(256) k_match_query_warp(MatchArgs a, int /*split*/) {
     const int pair = blockIdx.y;
     const int qs = a.qslot0 + pair, ts = a.tslot0 + pair;
     const int nq = a.counts[qs], nt = a.counts[ts];
@@ -66,8 +83,8 @@ __global__ void __launch_bounds__(256) k_match_query(MatchArgs a) {
     const int W = (a.n_d + 63) / 64;
     const uint64_t* tkeys = a.keys + static_cast<size_t>(ts) * a.cap * a.tables;
     const uint64_t* tdesc = a.desc + static_cast<size_t>(ts) * a.cap * 2 * W;
-    const int q_base = (blockIdx.x * (blockDim.x >> 5) + warp) * kQueriesPerWarp;
-    for (int qq = 0; qq < kQueriesPerWarp; ++qq) {
+    const int q_base = blockIdx.x * (blockDim.x >> 5) + warp;
+    for (int qq = 0; qq < 1; ++qq) {
         const int q = q_base + qq;
         if (q >= nq) return;
         uint64_t qk[8];
@@ -109,6 +126,83 @@ __global__ void __launch_bounds__(256) k_match_query(MatchArgs a) {
             r.w = 0;
             a.qres[static_cast<size_t>(pair) * a.cap + q] = r;
         }
+    }
+}
+
+// `split` warps per query (2, 4 or 8; 8 / split queries per CTA), each
+// scanning every split-th block of 32 train descriptors: small problems put
+// more warps in flight and fewer serial load round trips on each; their
+// lexicographic top-2 lists merge in shared memory (the top-2 of
+// (distance, id) does not depend on the visiting order)
+__global__ void __launch_bounds__(256, 4) k_match_query_split(MatchArgs a, int split) {
+    __shared__ int4 s_top[8];
+    const int pair = blockIdx.y;
+    const int qs = a.qslot0 + pair, ts = a.tslot0 + pair;
+    const int nq = a.counts[qs], nt = a.counts[ts];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int part = warp % split;
+    const int W = (a.n_d + 63) / 64;
+    const uint64_t* tkeys = a.keys + static_cast<size_t>(ts) * a.cap * a.tables;
+    const uint64_t* tdesc = a.desc + static_cast<size_t>(ts) * a.cap * 2 * W;
+    const int q = blockIdx.x * (8 / split) + warp / split;
+    const int BIG = 0x7fffffff;
+    int d0 = BIG, j0 = BIG, d1 = BIG, j1 = BIG;
+    if (q < nq) {
+        // the query's keys stay in registers (a guarded full unroll: a runtime
+        // trip count would put them on the stack); its descriptor is read
+        // (L1) only for the few candidates
+        uint64_t qk[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            qk[t] = t < a.tables ? a.keys[(static_cast<size_t>(qs) * a.cap + q) * a.tables + t] : 0ull;
+        const uint64_t* qdp = a.desc + (static_cast<size_t>(qs) * a.cap + q) * 2 * W;
+        for (int j = 32 * part + lane; j < nt; j += 32 * split) {
+            bool cand = false;
+            if (a.tables <= 8) {
+                uint64_t tk[8];  // all of train j's keys in flight, then the tests
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    tk[t] = t < a.tables ? __ldg(tkeys + static_cast<size_t>(j) * a.tables + t) : 0ull;
+#pragma unroll
+                for (int t = 0; t < 8; ++t) cand = cand || (t < a.tables && in_probe_set(qk[t] ^ tk[t], a));
+            } else {
+                for (int t = 0; t < a.tables; ++t) {
+                    const uint64_t tk = tkeys[static_cast<size_t>(j) * a.tables + t];
+                    const uint64_t qkt = a.keys[(static_cast<size_t>(qs) * a.cap + q) * a.tables + t];
+                    if (in_probe_set(qkt ^ tk, a)) {
+                        cand = true;
+                        break;
+                    }
+                }
+            }
+            if (!cand) continue;
+            const uint64_t* td = tdesc + static_cast<size_t>(j) * 2 * W;
+            int d = 0;
+            for (int w = 0; w < 2 * W; ++w) d += __popcll(__ldg(qdp + w) ^ td[w]);
+            if (d <= a.max_distance) top2_insert(d, j, d0, j0, d1, j1);
+        }
+        // warp merge of the per-lane top-2 lists
+        for (int off = 16; off > 0; off >>= 1) {
+            int od0 = __shfl_xor_sync(0xffffffffu, d0, off), oj0 = __shfl_xor_sync(0xffffffffu, j0, off);
+            int od1 = __shfl_xor_sync(0xffffffffu, d1, off), oj1 = __shfl_xor_sync(0xffffffffu, j1, off);
+            top2_insert(od0, oj0, d0, j0, d1, j1);
+            top2_insert(od1, oj1, d0, j0, d1, j1);
+        }
+        if (lane == 0) s_top[warp] = make_int4(d0, j0, d1, j1);
+    }
+    __syncthreads();
+    if (q < nq && part == 0 && lane == 0) {
+        for (int k = 1; k < split; ++k) {
+            const int4 o = s_top[warp + k];
+            top2_insert(o.x, o.y, d0, j0, d1, j1);
+            top2_insert(o.z, o.w, d0, j0, d1, j1);
+        }
+        int4 r;
+        r.x = j0 == BIG ? -1 : j0;
+        r.y = d0;
+        r.z = j1 == BIG ? -1 : d1;  // second-best distance, or -1 when < 2 hits
+        r.w = 0;
+        a.qres[static_cast<size_t>(pair) * a.cap + q] = r;
     }
 }
 
@@ -185,9 +279,17 @@ void match_launch(const MatchArgs& a, cudaStream_t s) {
     if (a.npairs <= 0) return;
     if (a.n_d > 64 * kMaxW) throw Status(LP_BAD_PARAMS, "match: n_d too large");
     if (a.cap >= (1 << 21)) throw Status(LP_BAD_PARAMS, "match: too many descriptors");
-    LPB_LAUNCH(k_lsh_keys, cdiv(static_cast<long long>(a.nslots) * a.cap, 256), 256, 0, s, a);
-    dim3 grid(cdiv(a.cap, 8 * kQueriesPerWarp), a.npairs);
-    LPB_LAUNCH(k_match_query, grid, 256, 0, s, a);
+    if (a.bits > 64) throw Status(LP_BAD_PARAMS, "match: more than 64 key bits");
+    LPB_LAUNCH(k_lsh_keys, cdiv(static_cast<long long>(a.nslots) * a.cap * 32, 256), 256, 0, s, a);
+    // about 32 warps per SM in total: split the scans of small problems,
+    // keep one warp per query on large ones (setup per warp is the cost there)
+    const long long queries = static_cast<long long>(a.npairs) * a.cap;
+    int split = 1;
+    while (split < 8 && queries * split * 2 <= 148LL * 32) split <<= 1;
+    dim3 grid(cdiv(a.cap, 8 / split), a.npairs);
+    // one profiler key (k_match_query/0) for either kernel
+    auto* k_match_query = split > 1 ? &k_match_query_split : &k_match_query_warp;
+    LPB_LAUNCH(k_match_query, grid, 256, 0, s, a, split);
     int p2 = 1;
     while (p2 < a.cap) p2 <<= 1;
     const int smem = p2 * 4;
