@@ -93,6 +93,37 @@ __device__ void mt_twist_warp(Mt64& r) {
     }
     __syncwarp();
 }
+// the same draw with the state index in a register (the sampler's draws
+// then form a short dependency chain: one shared load + tempering each)
+__device__ __forceinline__ uint64_t mt_next_reg(Mt64& r, int& idx) {
+    if (idx >= 312) {
+        r.idx = idx;
+        const uint64_t y = mt_next(r);  // twists, then consumes word 0
+        idx = r.idx;
+        return y;
+    }
+    uint64_t y = r.mt[idx++];
+    y ^= (y >> 29) & 0x5555555555555555ull;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+    y ^= (y << 37) & 0xFFF7EEE000000000ull;
+    y ^= y >> 43;
+    return y;
+}
+__device__ __forceinline__ int uid_int_reg(Mt64& r, int& idx, int a, int b) {
+    const uint64_t range = static_cast<uint64_t>(static_cast<int64_t>(b)) -
+                           static_cast<uint64_t>(static_cast<int64_t>(a)) + 1ull;
+    uint64_t x = mt_next_reg(r, idx);
+    uint64_t low = x * range, high = __umul64hi(x, range);
+    if (low < range) {
+        const uint64_t thr = (0ull - range) % range;
+        while (low < thr) {
+            x = mt_next_reg(r, idx);
+            low = x * range;
+            high = __umul64hi(x, range);
+        }
+    }
+    return static_cast<int>(high + static_cast<uint64_t>(static_cast<int64_t>(a)));
+}
 __device__ int uid_int(Mt64& r, int a, int b) {
     const uint64_t range = static_cast<uint64_t>(static_cast<int64_t>(b)) -
                            static_cast<uint64_t>(static_cast<int64_t>(a)) + 1ull;
@@ -413,7 +444,8 @@ __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, dou
         }
         // hartley_normalizer centroids: sequential sums (homography.hpp:83-88)
         Norm ns{0, 0, 1}, nd{0, 0, 1};
-        for (int i = 0; i < m; ++i) {
+#pragma unroll 8
+        for (int i = 0; i < m; ++i) {  // loads run ahead; the adds stay in order
             const lp_corr c = P(i);
             ns.cx += c.sx;
             ns.cy += c.sy;
@@ -444,8 +476,11 @@ __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, dou
     __syncthreads();
     if (tid == 0) {  // mean distances: sequential sums (homography.hpp:89-95)
         double ms = 0, md = 0;
-        for (int i = 0; i < m; ++i) ms += terms[i];
-        for (int i = 0; i < m; ++i) md += terms[m + i];
+#pragma unroll 8
+        for (int i = 0; i < m; ++i) {  // two independent chains, one loop
+            ms += terms[i];
+            md += terms[m + i];
+        }
         ms /= static_cast<double>(m);
         md /= static_cast<double>(m);
         sh.ns.scale = ms > 1e-12 ? sqrt(2.0) / ms : 1.0;
@@ -659,16 +694,23 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
                     t_n = t_next;
                     ++pool;
                 }
+                // homography.hpp:212-222: four distinct indices by rejection
+                int idx = S.rng.idx, smp[4];
+#pragma unroll
                 for (int i = 0; i < 4; ++i)
                     for (;;) {
-                        int v = uid_int(S.rng, 0, pool - 1);
+                        const int v = uid_int_reg(S.rng, idx, 0, pool - 1);
                         bool dup = false;
-                        for (int j = 0; j < i; ++j) dup |= S.samples[h][j] == v;
+#pragma unroll
+                        for (int j = 0; j < i; ++j) dup |= smp[j] == v;
                         if (!dup) {
-                            S.samples[h][i] = v;
+                            smp[i] = v;
                             break;
                         }
                     }
+                S.rng.idx = idx;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) S.samples[h][i] = smp[i];
                 S.pools[h] = pool;
             }
         }
