@@ -60,6 +60,7 @@ void rectify_launch(const RectCam* cams, int ncams, int in_w, int in_h, int max_
 
 // Full per-frame compositor: warp, coverage runs, pyramids, band blend + collapse.
 void compose_launch(const ComposeArgs& a, cudaStream_t s);
+const void* warp_kernel_fn();  // k_warp, for patching its node in a captured chain
 // Pyramid + blend + collapse only (level-0 images and masks already in G/M).
 void blend_launch(const ComposeArgs& a, cudaStream_t s);
 

@@ -457,3 +457,29 @@ def test_rig_nondefault_params_generic_paths(lp, orc):
         assert np.array_equal(got["matches"][q], want["matches"][q]), q
     assert np.array_equal(got["homographies"], want["homographies"])
     assert np.array_equal(got["panorama"], want["panorama"])
+
+
+def test_rig_refresh_every_frame_graph_updates(lp, orc):
+    """Re-registration on every frame with device-resident inputs (estimate on
+    the feature stream) and CUDA graphs: homographies that change below a
+    pixel of canvas patch the k_warp node in place, a different overlap moves
+    the canvas (graph recapture + in-place update); every panorama equals the
+    oracle's stitch_frame for that frame and the direct-launch rig's."""
+    import torch
+    from paper_1810_03988_b200 import Rig
+    p = orc.default_params()
+    p.seed = p.matching.seed = 42
+    p.homography_refresh = 1
+    frames = [orc.sequence_frame(400, 300, t, 0.25, 42) for t in range(5)]
+    l2, r2, _ = orc.planted_pair(400, 300, 0.3, 7)
+    frames += [(l2, r2)] + [orc.sequence_frame(400, 300, t, 0.25, 42) for t in range(5, 8)]
+    direct = Rig(lp, 2, 400, 300, p)
+    direct.set_graphs(False)
+    graph = Rig(lp, 2, 400, 300, p)
+    for t, (l, r) in enumerate(frames):
+        want = orc.stitch_frame([l, r], p, frame_index=t)["panorama"]
+        a = direct.stitch([l, r], t)["panorama"]
+        dev = [torch.from_numpy(l).cuda(), torch.from_numpy(r).cuda()]
+        b = graph.stitch(dev, t)["panorama"]
+        assert np.array_equal(a, want), t
+        assert np.array_equal(b, want), t
