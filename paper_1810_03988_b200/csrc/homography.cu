@@ -16,6 +16,7 @@
 //    Householder QR with the canonical 256-lane blocked dot product, then the
 //    warp Jacobi SVD of the 9x9 factor.
 // Compiled with --fmad=false: every FP64 expression rounds like the x86 oracle.
+#include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 
 #include "homography.cuh"
@@ -625,7 +626,11 @@ __device__ int block_compact(int n, int* idx, F flag) {
     return base;
 }
 
-constexpr int kChunk = 8;  // hypotheses per round = warps per CTA
+constexpr int kChunk = 8;  // hypotheses per round = warps per CTA (or CTAs per cluster)
+__device__ __forceinline__ double* s_dyn_refit() {
+    extern __shared__ __align__(16) double s_dyn[];
+    return s_dyn;
+}
 
 struct ProsacShared {
     Mt64 rng;
@@ -640,21 +645,41 @@ struct ProsacShared {
     uint8_t in[kChunk][32];
     double best_h[9], best_hi[9];
     int best_count, iterations, done, final_count;
+    // cluster mode: hypothesis h of a round is scored by cluster rank h,
+    // which writes its verdict here in rank 0's shared memory (DSMEM)
+    struct Verdict {
+        int valid, cnt;
+        double err;
+        double h[9], hi[9];
+    } rres[kChunk];
+    int c_ok, c_cnt;
+    double c_err;
     double H[9], Hi[9];
     int refit_ok;
     RefitShared refit;
 };
 
+// Launched either as one CTA per pair (8 hypotheses per round, one warp
+// each) or as a cluster of kChunk CTAs per pair: every rank runs the same
+// deterministic sampler, rank h takes hypothesis h of the round (its 4-point
+// DLT on warp 0 without FP64 contention from the others, the scoring by the
+// whole CTA), verdicts meet in rank 0's shared memory, rank 0 decides and
+// refits. Same hypotheses, same order of decisions, same sums: same result.
 __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
     __shared__ ProsacShared S;
-    const int pair = blockIdx.x;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int nr = static_cast<int>(cl.num_blocks());
+    const bool clustered = nr == kChunk;
+    const int rank = clustered ? static_cast<int>(cl.block_rank()) : 0;
+    const int pair = clustered ? static_cast<int>(blockIdx.x) / kChunk : static_cast<int>(blockIdx.x);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (a.pair_status[pair] != LP_OK) return;
     PTRACE("start");
     const int n = a.counts[pair];
     const lp_corr* m = a.corr + static_cast<size_t>(pair) * a.cap;
     if (n < 4) {
-        if (tid == 0) {
+        if (tid == 0 && rank == 0) {
             a.pair_status[pair] = LP_INSUFFICIENT_MATCHES;
             a.iterations[pair] = 0;
         }
@@ -683,6 +708,9 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
     __syncthreads();
     PTRACE("twisted");
     const int* exit_row = a.exit_tab + (a.nmax > 0 ? static_cast<size_t>(n) * (a.nmax + 1) : 0);
+    // cluster mode needs every error of a hypothesis in shared memory
+    const bool cmode = clustered && n <= 27 * a.smem_rows;
+    if (clustered && !cmode && rank != 0) return;  // rank 0 alone, one warp per hypothesis
     for (int t0 = 1; t0 <= a.max_iter; t0 += kChunk) {
         const int chunk = min(kChunk, a.max_iter - t0 + 1);
         if (tid == 0) {
@@ -716,7 +744,76 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
         }
         __syncthreads();
         PTRACE("sampled");
-        if (warp < chunk) {
+        if (cmode) {
+            if (rank < chunk) {
+                double H[9], Hi[9];
+                if (warp == 0) {
+                    lp_corr q[4];
+                    for (int i = 0; i < 4; ++i) q[i] = m[S.samples[rank][i]];
+                    const bool ok = dlt_minimal_warp(q, H) == LP_OK && h_inverse(H, Hi);
+                    if (lane == 0) {
+                        S.c_ok = ok;
+                        for (int i = 0; i < 9; ++i) {
+                            S.h[0][i] = H[i];
+                            S.hi[0][i] = Hi[i];
+                        }
+                    }
+                }
+                __syncthreads();
+                const bool ok = S.c_ok;
+                for (int i = 0; i < 9; ++i) {
+                    H[i] = S.h[0][i];
+                    Hi[i] = S.hi[0][i];
+                }
+                if (ok) {
+                    // errors of all correspondences in parallel (-1: outlier),
+                    // then the count and the in-order error sum
+                    // (homography.hpp:240-247) by thread 0
+                    double* se = s_dyn_refit();
+                    for (int i = tid; i < n; i += 256) {
+                        const double e = ste(H, Hi, m[i]);
+                        se[i] = e <= a.threshold ? e : -1.0;
+                    }
+                    __syncthreads();
+                    if (tid == 0) {
+                        int count = 0;
+                        double err = 0.0;
+                        for (int i = 0; i < n; ++i) {
+                            const double v = se[i];
+                            if (v >= 0.0) {
+                                ++count;
+                                err += v;
+                            }
+                        }
+                        S.c_cnt = count;
+                        S.c_err = err;
+                    }
+                    __syncthreads();
+                }
+                if (tid == 0) {
+                    ProsacShared::Verdict* v = cl.map_shared_rank(&S.rres[rank], 0);
+                    v->valid = ok;
+                    v->cnt = ok ? S.c_cnt : 0;
+                    v->err = ok ? S.c_err : 0.0;
+                    for (int i = 0; i < 9; ++i) {
+                        v->h[i] = H[i];
+                        v->hi[i] = Hi[i];
+                    }
+                }
+            }
+            cl.sync();
+            if (rank == 0 && tid == 0) {
+                for (int h = 0; h < chunk; ++h) {
+                    S.valid[h] = S.rres[h].valid;
+                    S.cnt[h] = S.rres[h].cnt;
+                    S.err[h] = S.rres[h].err;
+                    for (int i = 0; i < 9; ++i) {
+                        S.h[h][i] = S.rres[h].h[i];
+                        S.hi[h][i] = S.rres[h].hi[i];
+                    }
+                }
+            }
+        } else if (warp < chunk) {
             lp_corr q[4];
             for (int i = 0; i < 4; ++i) q[i] = m[S.samples[warp][i]];
             double H[9], Hi[9];
@@ -756,7 +853,7 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
         }
         __syncthreads();
         PTRACE("scored");
-        if (tid == 0) {
+        if (tid == 0 && rank == 0) {
             for (int h = 0; h < chunk; ++h) {
                 const int t = t0 + h;
                 if (a.trace_pool) a.trace_pool[static_cast<size_t>(pair) * a.max_iter + t - 1] = S.pools[h];
@@ -782,7 +879,20 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
             }
         }
         __syncthreads();
-        if (S.done) break;
+        if (cmode) {
+            cl.sync();  // rank 0's decision is complete
+            if (tid == 0) S.c_ok = *cl.map_shared_rank(&S.done, 0);
+            __syncthreads();
+            if (S.c_ok) break;
+        } else if (S.done) {
+            break;
+        }
+    }
+    if (cmode) {
+        // every rank has read rank 0's verdict; only rank 0 goes on (no rank
+        // reads another's shared memory after this point)
+        cl.sync();
+        if (rank != 0) return;
     }
     if (S.best_count < 4) {
         if (tid == 0) {
@@ -809,7 +919,7 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
     if (n_in <= a.smem_rows) {
         // the inliers and the whole refit system in shared memory: the
         // sequential Hartley sums and the blocked QR passes read on-chip
-        extern __shared__ __align__(16) double s_refit[];
+        double* s_refit = s_dyn_refit();
         double* sA = s_refit;                                        // 2 n_in x 9
         double* sv = sA + static_cast<size_t>(2 * a.smem_rows) * 9;  // 2 n_in
         double* st_terms = sv + 2 * a.smem_rows;                     // 2 n_in
@@ -861,7 +971,31 @@ void prosac_launch(const ProsacArgs& a0, cudaStream_t s) {
     a.smem_rows = std::min(a.cap, kRefitSmemRows);
     const int smem = a.smem_rows * static_cast<int>(2 * 9 * 8 + 2 * 8 + 2 * 8 + sizeof(lp_corr));
     ensure_dyn_smem(reinterpret_cast<const void*>(&k_prosac), smem);
-    LPB_LAUNCH(k_prosac, a.npairs, 256, smem, s, a);
+    // a cluster of kChunk CTAs per pair (LPB_PROSAC_CLUSTER=0: one CTA)
+    static const bool use_cluster = [] {
+        const char* e = std::getenv("LPB_PROSAC_CLUSTER");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    if (!use_cluster) {
+        LPB_LAUNCH(k_prosac, a.npairs, 256, smem, s, a);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.npairs * kChunk);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kChunk;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const int pt = prof_begin("k_prosac", s);
+    LPB_CUDA(cudaLaunchKernelEx(&cfg, k_prosac, a));
+    prof_end(pt, s);
+    note_launch();
 }
 
 __global__ void k_chain(const lp_homography* ph, const int* pst, int npairs, lp_homography* chain,
