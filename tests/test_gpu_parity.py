@@ -483,3 +483,35 @@ def test_rig_refresh_every_frame_graph_updates(lp, orc):
         b = graph.stitch(dev, t)["panorama"]
         assert np.array_equal(a, want), t
         assert np.array_equal(b, want), t
+
+
+def test_prosac_single_cta_path_matches(tmp_path):
+    """PROSAC's one-CTA launch (LPB_PROSAC_CLUSTER=0, also the in-kernel
+    fallback for very large correspondence sets) against the oracle, in a
+    fresh process (the launch mode is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import sys
+sys.path.insert(0, %r)
+import numpy as np
+from oracle import Oracle
+from paper_1810_03988_b200 import Lorb
+from tests.golden.make_golden import prosac_data
+orc, lp = Oracle("orc"), Lorb(0)
+for seed in (1, 2):
+    src, dst, q = prosac_data(seed + 3, n=300, inlier_frac=0.5, noise=1.0)
+    corr = orc.corr_array(src, dst, q)
+    pc = orc.default_params().prosac
+    pc.seed = seed
+    a = lp.prosac_homography(corr, pc, trace=True)
+    b = orc.prosac_homography(corr, pc, trace=True)
+    assert a["iterations"] == b["iterations"] and np.array_equal(a["samples"], b["samples"])
+    assert np.array_equal(a["model"], b["model"]) and np.array_equal(a["mask"], b["mask"])
+print("ok")
+''' % root
+    env = dict(os.environ, LPB_PROSAC_CLUSTER="0")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stdout + out.stderr
