@@ -803,11 +803,26 @@ __global__ void __launch_bounds__(256) k_describe6(const __grid_constant__ Extra
         if (lane == 0) dev_fail(a.status, LP_PATCH_OUT_OF_BOUNDS);
         return;
     }
-    uint8_t* s_in = s_warp_base + static_cast<size_t>(warp) * warp_bytes;            // iw x iw u8
-    float* s_tmp = reinterpret_cast<float*>(s_in + ((iw * iw + 15) & ~15));          // iw x pw
+    const int rowb = (iw + 6) / 4 * 4;  // staged row pitch: the words covering a row at any alignment
+    uint8_t* s_in = s_warp_base + static_cast<size_t>(warp) * warp_bytes;            // iw x rowb u8
+    float* s_tmp = reinterpret_cast<float*>(s_in + ((iw * rowb + 15) & ~15));        // iw x pw
     const int bx = kp.x - P - D6_RB, by = kp.y - P - D6_RB;
+    // interior patches: the aligned words covering each row by cp.async, all
+    // in flight at once; patches at the image border: clamped byte loads
+    const int ax = bx & ~3, nw = (bx - ax + iw + 3) / 4;
+    const bool words = ax >= 0 && by >= 0 && ax + 4 * nw <= im.w && by + iw <= im.h && (im.w & 3) == 0 &&
+                       (reinterpret_cast<uintptr_t>(im.p) & 3) == 0;
+    const int spitch = words ? rowb : iw, soff = words ? bx - ax : 0;
+    if (words) {
+        uint32_t* s_w = reinterpret_cast<uint32_t*>(s_in);
+        for (int j = lane; j < iw * nw; j += 32) {
+            const int ly = j / nw, q = j - ly * nw;
+            cp_async4(s_w + ly * (rowb / 4) + q, im.p + static_cast<size_t>(by + ly) * im.w + ax + 4 * q, true);
+        }
+        cp_async_wait_all();
+    }
     // stage the u8 patch; 8 loads in flight per lane
-    for (int j0 = lane; j0 < iw * iw; j0 += 32 * 8) {
+    for (int j0 = lane; !words && j0 < iw * iw; j0 += 32 * 8) {
         uint8_t v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -829,7 +844,7 @@ __global__ void __launch_bounds__(256) k_describe6(const __grid_constant__ Extra
     const int pw2 = (pw + 1) / 2;
     for (int j = lane; j < iw * pw2; j += 32) {
         const int ly = j / pw2, lx = 2 * (j - ly * pw2);
-        const uint8_t* row = s_in + ly * iw + lx;
+        const uint8_t* row = s_in + ly * spitch + soff + lx;
         float v[2 * D6_RB + 2];
 #pragma unroll
         for (int q = 0; q < 2 * D6_RB + 2; ++q) v[q] = lx + q < iw ? static_cast<float>(row[q]) : 0.0f;
@@ -894,7 +909,8 @@ void extract_launch(const ExtractArgs& a, cudaStream_t s) {
     const int P = a.patch_half, RB = a.blur_r;
     const int pw = 2 * P + 1, iw = pw + 2 * RB;
     if (RB == D6_RB) {
-        const int warp_bytes6 = (((iw * iw + 15) & ~15) + iw * pw * 4 + 15) & ~15;
+        const int rowb6 = (iw + 6) / 4 * 4;  // k_describe6's staged row pitch
+        const int warp_bytes6 = (((iw * rowb6 + 15) & ~15) + iw * pw * 4 + 15) & ~15;
         const int head6 = (a.n_d * static_cast<int>(sizeof(lp_pair)) + 15) & ~15;
         int warps6 = 8;
         while (warps6 > 1 && head6 + warps6 * warp_bytes6 > 200 * 1024) warps6 >>= 1;
