@@ -993,7 +993,14 @@ void prosac_launch(const ProsacArgs& a0, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const int pt = prof_begin("k_prosac", s);
-    LPB_CUDA(cudaLaunchKernelEx(&cfg, k_prosac, a));
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_prosac, a);
+    if (e != cudaSuccess) {
+        // no room for an 8-CTA cluster (a partitioned or busy device): the
+        // one-CTA launch computes the same result
+        cudaGetLastError();
+        k_prosac<<<a.npairs, 256, smem, s>>>(a);
+        LPB_CUDA(cudaGetLastError());
+    }
     prof_end(pt, s);
     note_launch();
 }
