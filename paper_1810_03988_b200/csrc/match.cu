@@ -10,7 +10,7 @@
 // (distance, train_id) of one query, which is all the ratio test
 // (matchlsh.hpp:183-186) needs. A per-pair CTA then orders accepted matches by
 // (quality desc, query_id asc) = (distance asc, query_id asc) with a bitonic
-// sort and emits the Correspondence list for PROSAC (pipeline.hpp:480-488).
+// rank placement and emits the Correspondence list for PROSAC (pipeline.hpp:480-488).
 #include "match.cuh"
 
 namespace lpb {
@@ -231,46 +231,32 @@ __global__ void __launch_bounds__(1024) k_match_finalize(MatchArgs a) {
     }
     __syncthreads();
     const int n = s_n;
-    int p2 = 1;
-    while (p2 < n) p2 <<= 1;
-    for (int i = n + threadIdx.x; i < p2; i += blockDim.x) s_k[i] = 0xffffffffu;
-    __syncthreads();
-    for (int k = 2; k <= p2; k <<= 1)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < p2; i += blockDim.x) {
-                int p = i ^ j;
-                if (p > i) {
-                    uint32_t x = s_k[i], y = s_k[p];
-                    bool asc = (i & k) == 0;
-                    if (asc ? (x > y) : (x < y)) {
-                        s_k[i] = y;
-                        s_k[p] = x;
-                    }
-                }
-            }
-            __syncthreads();
-        }
+    // (distance, query) keys are unique: each accepted match goes straight to
+    // its rank in ascending order (matchlsh.hpp:188-191), no sorting network
     const float denom = fmul(2.0f, static_cast<float>(a.n_d));
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int q = static_cast<int>(s_k[i] & 0x1FFFFFu);
-        const int d = static_cast<int>(s_k[i] >> 21);
-        const int4 r = a.qres[static_cast<size_t>(pair) * a.cap + q];
+        const uint32_t key = s_k[i];
+        int r = 0;
+        for (int j = 0; j < n; ++j) r += s_k[j] < key;
+        const int q = static_cast<int>(key & 0x1FFFFFu);
+        const int d = static_cast<int>(key >> 21);
+        const int4 qr = a.qres[static_cast<size_t>(pair) * a.cap + q];
         lp_match m;
         m.query_id = q;
-        m.train_id = r.x;
+        m.train_id = qr.x;
         m.distance = d;
         m.quality = fsub(1.0f, __fdiv_rn(static_cast<float>(d), denom));
-        a.matches[static_cast<size_t>(pair) * a.cap + i] = m;
-        const lp_keypoint s = a.kps[static_cast<size_t>(qs) * a.cap + q];
-        const lp_keypoint t = a.kps[static_cast<size_t>(ts) * a.cap + r.x];
+        a.matches[static_cast<size_t>(pair) * a.cap + r] = m;
+        const lp_keypoint sk = a.kps[static_cast<size_t>(qs) * a.cap + q];
+        const lp_keypoint tk = a.kps[static_cast<size_t>(ts) * a.cap + qr.x];
         lp_corr c;
-        c.sx = static_cast<double>(s.x);
-        c.sy = static_cast<double>(s.y);
-        c.dx = static_cast<double>(t.x);
-        c.dy = static_cast<double>(t.y);
+        c.sx = static_cast<double>(sk.x);
+        c.sy = static_cast<double>(sk.y);
+        c.dx = static_cast<double>(tk.x);
+        c.dy = static_cast<double>(tk.y);
         c.quality = m.quality;
         c.pad_ = 0;
-        a.corr[static_cast<size_t>(pair) * a.cap + i] = c;
+        a.corr[static_cast<size_t>(pair) * a.cap + r] = c;
     }
     if (threadIdx.x == 0) a.match_counts[pair] = n;
 }
