@@ -9,8 +9,8 @@
 // (matchlsh.hpp:25-33), and each warp keeps the lexicographic top-2
 // (distance, train_id) of one query, which is all the ratio test
 // (matchlsh.hpp:183-186) needs. A per-pair CTA then orders accepted matches by
-// (quality desc, query_id asc) = (distance asc, query_id asc) with a bitonic
-// rank placement and emits the Correspondence list for PROSAC (pipeline.hpp:480-488).
+// (quality desc, query_id asc) = (distance asc, query_id asc) by rank
+// placement and emits the Correspondence list for PROSAC (pipeline.hpp:480-488).
 #include "match.cuh"
 
 namespace lpb {
