@@ -6,7 +6,7 @@
 # usage: TAG=v7 bash scripts/profile_round.sh
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-TAG=${TAG:-v8}
+TAG=${TAG:-v10}
 export LPB_GRAPHS=0   # individual launches (graph nodes are otherwise one launch)
 [ "${SKIP_LAUNCHES:-0}" = "1" ] || timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches_cfg3_$TAG.csv python bench.py --steps 2 --warmup 1 --no-e2e \
