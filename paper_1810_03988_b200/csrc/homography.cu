@@ -665,7 +665,7 @@ struct ProsacShared {
 // DLT on warp 0 without FP64 contention from the others, the scoring by the
 // whole CTA), verdicts meet in rank 0's shared memory, rank 0 decides and
 // refits. Same hypotheses, same order of decisions, same sums: same result.
-__global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
+__device__ __forceinline__ void prosac_body(const ProsacArgs& a) {
     __shared__ ProsacShared S;
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
@@ -965,6 +965,8 @@ __global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
     }
 }
 
+__global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a);
+
 void prosac_launch(const ProsacArgs& a0, cudaStream_t s) {
     ProsacArgs a = a0;
     // refit rows kept on chip: 2 rows x 9 + 2 + 2 doubles and one lp_corr per inlier
@@ -1005,9 +1007,10 @@ void prosac_launch(const ProsacArgs& a0, cudaStream_t s) {
     note_launch();
 }
 
-__global__ void k_chain(const lp_homography* ph, const int* pst, int npairs, lp_homography* chain,
-                        int* chain_status) {
-    if (threadIdx.x != 0) return;
+// HomographyCache chain (pipeline.hpp:474-494): chain[0] = I, chain[i+1] =
+// chain[i] * H_pair(i), renormalised by h33; first failing pair's status wins
+__device__ void chain_compose(const lp_homography* ph, const int* pst, int npairs, lp_homography* chain,
+                              int* chain_status) {
     int st = LP_OK;
     for (int i = 0; i < npairs; ++i)
         if (pst[i] != LP_OK && st == LP_OK) st = pst[i];
@@ -1033,6 +1036,26 @@ __global__ void k_chain(const lp_homography* ph, const int* pst, int npairs, lp_
             c[i] = o[i];
             chain[p + 1].h[i] = o[i];
         }
+    }
+}
+
+__global__ void k_chain(const lp_homography* ph, const int* pst, int npairs, lp_homography* chain,
+                        int* chain_status) {
+    if (threadIdx.x == 0) chain_compose(ph, pst, npairs, chain, chain_status);
+}
+
+__global__ void __launch_bounds__(256, 1) k_prosac(ProsacArgs a) {
+    prosac_body(a);
+    if (!a.chain_counter || threadIdx.x != 0) return;
+    namespace cg = cooperative_groups;
+    const cg::cluster_group cl = cg::this_cluster();
+    if (cl.num_blocks() > 1 && cl.block_rank() != 0) return;
+    // every pair's verdict is final: the last one composes the chain
+    __threadfence();
+    if (atomicAdd(a.chain_counter, 1u) == static_cast<unsigned>(a.npairs - 1)) {
+        __threadfence();
+        chain_compose(a.model, a.pair_status, a.npairs, a.chain, a.chain_status);
+        *a.chain_counter = 0u;
     }
 }
 

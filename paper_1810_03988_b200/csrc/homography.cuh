@@ -27,6 +27,11 @@ struct ProsacArgs {
     int* trace_samples;         // npairs * max_iter * 4 (optional)
     int* pair_status;           // npairs: in = upstream status (0 ok), out = PROSAC status
     int smem_rows;              // set by prosac_launch: refits with <= this many inliers run in shared memory
+    // optional: the last pair to finish composes the camera chain
+    // (pipeline.hpp:474-494) in the same launch; counter zero on entry
+    lp_homography* chain;       // npairs + 1
+    int* chain_status;
+    unsigned* chain_counter;
 };
 
 constexpr int kRefitSmemRows = 800;  // 800 x 232 B = 186 KB of dynamic shared memory
