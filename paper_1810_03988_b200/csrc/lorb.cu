@@ -766,7 +766,7 @@ __global__ void __launch_bounds__(256) k_describe(ExtractArgs a, int warp_bytes)
 // crop blur (imgops.hpp:50-72), so the descriptor is bit-identical while 512
 // instead of 961 vertical sums are formed and no 31x31 plane is stored
 // (7 KB of shared memory per warp instead of 11 KB).
-constexpr int D6_RB = 6;
+constexpr int D6_RB = kDescribeFastBlurR;
 __global__ void __launch_bounds__(256) k_describe6(const __grid_constant__ ExtractArgs a, int warp_bytes) {
     extern __shared__ __align__(16) unsigned char s_dyn[];
     lp_pair* s_pairs = reinterpret_cast<lp_pair*>(s_dyn);
@@ -882,9 +882,36 @@ __global__ void __launch_bounds__(256) k_describe6(const __grid_constant__ Extra
             g[h] = __ballot_sync(0xffffffffu, gt);
             l[h] = __ballot_sync(0xffffffffu, lt);
         }
+        const uint64_t gw = static_cast<uint64_t>(g[0]) | (static_cast<uint64_t>(g[1]) << 32);
+        const uint64_t lw = static_cast<uint64_t>(l[0]) | (static_cast<uint64_t>(l[1]) << 32);
         if (lane == 0) {
-            d[w] = static_cast<uint64_t>(g[0]) | (static_cast<uint64_t>(g[1]) << 32);
-            d[W + w] = static_cast<uint64_t>(l[0]) | (static_cast<uint64_t>(l[1]) << 32);
+            d[w] = gw;
+            d[W + w] = lw;
+        }
+        if (a.lsh_keys && lane == 0) {  // the words again for the key bits (the u8 patch is done with)
+            reinterpret_cast<uint64_t*>(s_in)[w] = gw;
+            reinterpret_cast<uint64_t*>(s_in)[W + w] = lw;
+        }
+    }
+    if (a.lsh_keys) {
+        // lane b builds bit b of every table's key; a ballot assembles it
+        // (the same bits k_lsh_keys extracts, matchlsh.hpp:70-80)
+        __syncwarp();
+        const uint64_t* dw = reinterpret_cast<const uint64_t*>(s_in);
+        uint64_t* out = a.lsh_keys + (static_cast<size_t>(rg.out_slot) * a.cap_slot + idx) * a.lsh_tables;
+        for (int t = 0; t < a.lsh_tables; ++t) {
+            uint64_t key = 0;
+            for (int b0 = 0; b0 < a.lsh_bits; b0 += 32) {
+                const int b = b0 + lane;
+                unsigned v = 0;
+                if (b < a.lsh_bits) {
+                    const int p = __ldg(a.lsh_bitpos + t * a.lsh_bits + b);
+                    const int q = p < a.n_d ? p : p - a.n_d;
+                    v = static_cast<unsigned>((dw[(p < a.n_d ? 0 : W) + (q >> 6)] >> (q & 63)) & 1ull);
+                }
+                key |= static_cast<uint64_t>(__ballot_sync(0xffffffffu, v)) << b0;
+            }
+            if (lane == 0) out[t] = key;
         }
     }
     if (lane == 0) a.kp_out[static_cast<size_t>(rg.out_slot) * a.cap_slot + idx] = kp;

@@ -19,6 +19,7 @@ constexpr int kDetTileY = 32;    // (rows)
 constexpr int kMaxHarrisR = 6;   // harris_sigma <= 2 (radius ceil(3 sigma))
 constexpr int kMaxBlurR = 12;    // brief_blur_sigma <= 4
 constexpr int kTopnSortCap = 8192;
+constexpr int kDescribeFastBlurR = 6;  // k_describe6's blur radius (sigma = 2)
 constexpr int kTopnRankCap = 2048;   // k_topn fast path: rank placement of <= 2048 keys
 constexpr int kTopnHistBins = 4096;  // first radix digit: top 12 key bits
 
@@ -51,6 +52,11 @@ struct ExtractArgs {
     int cap_slot;
     int* slot_count;         // nslots
     int* status;             // device status word
+    // optional (k_describe6): the LSH keys of every descriptor (hash_key,
+    // matchlsh.hpp:70-80) in the matcher's layout, nslots * cap_slot * tables
+    uint64_t* lsh_keys;
+    const int* lsh_bitpos;   // tables * bits
+    int lsh_tables, lsh_bits;
 };
 
 // stage_detect + stage_describe for every region of every image in 4 launches

@@ -266,7 +266,8 @@ void match_launch(const MatchArgs& a, cudaStream_t s) {
     if (a.n_d > 64 * kMaxW) throw Status(LP_BAD_PARAMS, "match: n_d too large");
     if (a.cap >= (1 << 21)) throw Status(LP_BAD_PARAMS, "match: too many descriptors");
     if (a.bits > 64) throw Status(LP_BAD_PARAMS, "match: more than 64 key bits");
-    LPB_LAUNCH(k_lsh_keys, cdiv(static_cast<long long>(a.nslots) * a.cap * 32, 256), 256, 0, s, a);
+    if (!a.keys_ready)
+        LPB_LAUNCH(k_lsh_keys, cdiv(static_cast<long long>(a.nslots) * a.cap * 32, 256), 256, 0, s, a);
     // about 32 warps per SM in total: split the scans of small problems,
     // keep one warp per query on large ones (setup per warp is the cost there)
     const long long queries = static_cast<long long>(a.npairs) * a.cap;

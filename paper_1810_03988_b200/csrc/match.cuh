@@ -25,6 +25,7 @@ struct MatchArgs {
     lp_corr* corr;              // npairs * cap
     int* match_counts;          // npairs
     int* pair_status;           // npairs
+    int keys_ready;             // the extractor already wrote `keys` (k_describe6)
 };
 
 void match_launch(const MatchArgs& a, cudaStream_t s);
