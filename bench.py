@@ -281,9 +281,23 @@ def measured_peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def cpu_baseline(frames, params_fn, sample_frames=1):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline(frames, params_fn, sample_frames=1, pipelined_frames=4):
     """The reference CPU engine (oracle/_ref) on a bounded sample of the same
-    workload: `sample_frames` frames, serial StitchEngine, 1 core."""
+    workload: `sample_frames` frames through the serial StitchEngine on 1 core
+    (mode i), then `pipelined_frames` frames through its Pipelined mode with
+    frames_in_flight 4 and workers_per_stage = #cameras (mode ii,
+    pipeline.hpp:660-711). Returns (baseline dict, the serial run's panorama
+    as (H, W) u8 or None): the panorama is the parity check of the GPU arm."""
     import oracle
     from oracle import Oracle
     kind = "reference" if oracle.ref_available() else "port"
@@ -291,28 +305,51 @@ def cpu_baseline(frames, params_fn, sample_frames=1):
     p = params_fn(o)
     ncams = len(frames)
     h, w = frames[0].shape
+    stage_names = ["ingest", "rectify_crop", "detect", "describe", "match_estimate", "warp_blend", "output"]
+    pano = None
+    pipelined = None
     t0 = time.perf_counter()
     if kind == "reference":
         from paper_1810_03988_b200 import abi
         arr = (C.c_void_p * ncams)(*[f.ctypes.data for f in frames])
         fps, ms = C.c_double(), (C.c_double * 7)()
-        st = o.lib.ref_run_engine(ncams, w, h, C.byref(p), arr, sample_frames, 0, 1, 1,
-                                  C.byref(fps), ms)
+        cap = ncams * w * 2 * h
+        buf = np.zeros(cap, np.uint8)
+        cv = abi.Canvas()
+        fn = o.lib.ref_run_engine_out
+        fn.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+        st = fn(ncams, w, h, C.byref(p), arr, sample_frames, 0, 1, 1, C.byref(fps), ms,
+                buf.ctypes.data, cap, C.byref(cv))
         if st:
             raise abi.LorbError(st, o.lib.ref_last_error().decode())
         value = fps.value
-        stages = {n: round(ms[i], 2) for i, n in enumerate(
-            ["ingest", "rectify_crop", "detect", "describe", "match_estimate", "warp_blend",
-             "output"])}
+        serial_s = time.perf_counter() - t0
+        stages = {n: round(ms[i], 2) for i, n in enumerate(stage_names)}
+        pano = buf[:cv.width * cv.height].reshape(cv.height, cv.width).copy()
+        if pipelined_frames > 0:
+            workers = ncams
+            t1 = time.perf_counter()
+            st = fn(ncams, w, h, C.byref(p), arr, pipelined_frames, 1, 4, workers, C.byref(fps), ms,
+                    None, 0, None)
+            if st:
+                raise abi.LorbError(st, o.lib.ref_last_error().decode())
+            pipelined = {"value": fps.value, "unit": "frames/s", "mode": "Pipelined",
+                         "frames_in_flight": 4, "workers_per_stage": workers,
+                         "cores": min(os.cpu_count() or 1, 7 * workers),
+                         "sample": f"{pipelined_frames} frames, {time.perf_counter() - t1:.1f} s",
+                         "stage_ms": {n: round(ms[i], 2) for i, n in enumerate(stage_names)}}
     else:
         for _ in range(sample_frames):
             o.stitch_frame(frames, p)
         value = sample_frames / (time.perf_counter() - t0)
+        serial_s = time.perf_counter() - t0
         stages = None
-    return {"value": value, "unit": "frames/s", "cores": 1, "kind": kind,
-            "sample": f"{sample_frames} frame(s) of the same workload through the reference's "
-                      f"serial StitchEngine (pipeline.hpp:645-658), {time.perf_counter() - t0:.1f} s",
-            "stage_ms": stages}
+    return ({"value": value, "unit": "frames/s", "cores": 1, "kind": kind,
+             "sample": f"{sample_frames} frame(s) of the same workload through the reference's "
+                       f"serial StitchEngine (pipeline.hpp:645-658), {serial_s:.1f} s",
+             "stage_ms": stages, "pipelined": pipelined, "cpu_model": cpu_model(),
+             "host_threads": os.cpu_count()}, pano)
 
 
 def run_reference(args, cfgd):
@@ -378,6 +415,12 @@ def main():
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     args = ap.parse_args()
     cfgd = CONFIGS[args.config]
+    # `python bench.py --gpus N` without torchrun: launch the N ranks here
+    # (one process per GPU, torch.distributed.run on 127.0.0.1)
+    from paper_1810_03988_b200.shard import maybe_self_launch
+    rc = maybe_self_launch(os.path.abspath(__file__), sys.argv[1:], args.gpus)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args, cfgd)
 
@@ -390,12 +433,19 @@ def main():
     # driver's runs use one GPU per rank over NCCL
     if os.environ.get("LPB_RANKS_ON_ONE_GPU") == "1":
         local = 0
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
         backend = os.environ.get("LPB_DIST_BACKEND", "nccl")
         if backend == "nccl":
+            # communicator log (comm init lines carry nRanks) on stderr, so
+            # stdout keeps the single JSON line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
@@ -582,13 +632,23 @@ def main():
                      "basis": "SURVEY 8(d) B_frame at the device frame rate"}
 
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         def params_fn(o):
             q = o.default_params()
             q.seed = q.matching.seed = 42
             q.homography_refresh = cfgd["refresh"]
             return q
-        cpu = cpu_baseline(sets[0], params_fn, 1)
+        cpu, ref_pano = cpu_baseline(sets[0], params_fn, 1)
+        # parity of the measured path: the GPU rig's panorama of sets[0] at
+        # frame 0 (an estimating frame, as the reference engine's first)
+        # against the reference engine's panorama of the same frame
+        if ref_pano is not None:
+            got = rig.stitch(sets[0], 0)["panorama"]
+            parity = {"equal": bool(got.shape == ref_pano.shape and np.array_equal(got, ref_pano)),
+                      "max_abs_diff": int(np.abs(got.astype(int) - ref_pano.astype(int)).max())
+                      if got.shape == ref_pano.shape else None,
+                      "shape": list(got.shape), "against": "reference StitchEngine (oracle/_ref), frame 0 of set 0"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
@@ -600,7 +660,7 @@ def main():
                            "l2": f"{nsets} rotating input frame sets ({nsets * ncams * w * h / 1e6:.0f} MB) > 126 MB L2",
                            "parallelism": f"replicas x{world} (independent rigs, no data-path collective)"},
                 "gpu_launches": int(launches), "clocks": clk, "roofline": roofline,
-                "cpu_baseline": cpu, "e2e": e2e, "stage_ms": stage_ms if not args.no_profile else None,
+                "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "stage_ms": stage_ms if not args.no_profile else None,
                 "frame_hbm": frame_hbm, "kernel_ms": stage, "rank_checksums": checksums}
         s = json.dumps(line)
         print(s)

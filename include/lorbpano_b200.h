@@ -290,6 +290,13 @@ lp_status lp_rig_stitch(lp_rig* rig, const uint8_t* const* images, uint64_t fram
  * profiler names them) moves for the rig's last frame; < 0 if unknown. */
 double lp_rig_algorithmic_bytes(lp_rig* rig, const char* kernel_key);
 
+/* Failure injection (tests of the per-frame failure path): the frame
+ * submitted with `frame_index` raises device status `code` on its slot, as a
+ * kernel of that frame would; lp_rig_wait on its ticket returns `code`, the
+ * rig's other frames are unaffected (pipeline.hpp run_stage: a failed stage
+ * drops its frame into Metrics::drops and the engine carries on). */
+lp_status lp_rig_inject_fault(lp_rig* rig, uint64_t frame_index, int code);
+
 /* ---- diagnostics: per-kernel device time (CUDA events around each launch) ---- */
 void lp_profile_enable(int on);
 void lp_profile_reset(void);

@@ -639,9 +639,25 @@ int ref_stitch_frame_layout(int ncams, int w, int h, const lp_camera* cams, cons
 // frame (pipeline.hpp:369-387). mode 0 = serial, 1 = pipelined. Reports the
 // reference's own Metrics (frames_out / wall_seconds, per-stage means in ms,
 // stage order of pipeline.hpp:26-34).
+int ref_run_engine_out(int ncams, int w, int h, const lp_params* params,
+                       const std::uint8_t* const* images, int nframes, int mode, int frames_in_flight,
+                       int workers_per_stage, double* fps, double* stage_ms_mean,
+                       std::uint8_t* pano, std::size_t pano_cap, lp_canvas* canvas);
+
 int ref_run_engine(int ncams, int w, int h, const lp_params* params,
                    const std::uint8_t* const* images, int nframes, int mode, int frames_in_flight,
                    int workers_per_stage, double* fps, double* stage_ms_mean) {
+    return ref_run_engine_out(ncams, w, h, params, images, nframes, mode, frames_in_flight,
+                              workers_per_stage, fps, stage_ms_mean, nullptr, 0, nullptr);
+}
+
+// As ref_run_engine, and the last frame's composite leaves through the sink
+// (pipeline.hpp:369-387 FrameSink) into `pano` (canvas dims into `canvas`):
+// bench.py compares it with the GPU rig's panorama of the same frame.
+int ref_run_engine_out(int ncams, int w, int h, const lp_params* params,
+                       const std::uint8_t* const* images, int nframes, int mode, int frames_in_flight,
+                       int workers_per_stage, double* fps, double* stage_ms_mean,
+                       std::uint8_t* pano, std::size_t pano_cap, lp_canvas* canvas) {
     return guard([&] {
         PipelineConfig pc;
         pc.mode = mode ? PipelineMode::Pipelined : PipelineMode::Serial;
@@ -657,8 +673,18 @@ int ref_run_engine(int ncams, int w, int h, const lp_params* params,
             ++produced;
             return cams;
         };
-        FrameSink sink = [](const FramePacket&) {};
+        std::string sink_err;
+        FrameSink sink = [&](const FramePacket& pk) {
+            if (!pano) return;
+            if (pk.composite.data.size() > pano_cap) {
+                sink_err = "panorama capacity";
+                return;
+            }
+            std::memcpy(pano, pk.composite.data.data(), pk.composite.data.size());
+            if (canvas) *canvas = lp_canvas{pk.composite.width, pk.composite.height, 0, 0};
+        };
         Metrics m = eng.run(src, sink);
+        if (!sink_err.empty()) throw CapacityOverflow(sink_err);
         if (!m.drops.empty()) throw NumericalFailure("reference dropped a frame: " + m.drops[0].reason);
         *fps = m.frames_per_second;
         for (int s = 0; s < kNumStages; ++s) stage_ms_mean[s] = m.stage_summary(static_cast<Stage>(s)).mean / 1e6;

@@ -83,6 +83,8 @@ def load():
         lib.lp_rig_set_graphs.restype = C.c_int
         lib.lp_rig_set_streams.argtypes = [P, C.c_int]
         lib.lp_rig_set_streams.restype = C.c_int
+        lib.lp_rig_inject_fault.argtypes = [P, C.c_uint64, C.c_int]
+        lib.lp_rig_inject_fault.restype = C.c_int
         lib.lp_rig_algorithmic_bytes.argtypes = [P, C.c_char_p]
         lib.lp_rig_algorithmic_bytes.restype = C.c_double
         lib.lp_profile_enable.argtypes = [C.c_int]
@@ -194,6 +196,11 @@ class Rig:
     def set_graphs(self, on=True):
         """Replay the compositor chain as a CUDA graph per frame slot (default on)."""
         _check(self.lib, self.lib.lp_rig_set_graphs(self.rig, 1 if on else 0))
+
+    def inject_fault(self, frame_index, code):
+        """The frame submitted with `frame_index` fails with device status
+        `code` (lp_rig_inject_fault); only that frame's wait() raises."""
+        _check(self.lib, self.lib.lp_rig_inject_fault(self.rig, frame_index, code))
 
     def set_egress_rgb(self, on=True):
         """Panoramas leave the device as 3-channel RGB (the PPM sink's format)."""

@@ -50,3 +50,33 @@ def gather_results(res: RankResult, device=None):
 def aggregate_fps(total_frames, max_device_ms):
     """Whole-job throughput: frames of all ranks over the slowest rank's time."""
     return total_frames / (max_device_ms / 1e3) if max_device_ms > 0 else 0.0
+
+
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def torchrun_argv(script, argv, nproc, python=None, port=None):
+    """Command line that re-launches `script argv` as `nproc` ranks on this
+    node (one process per GPU), the way the driver launches multi-GPU runs:
+    torch.distributed.run, rendezvous on 127.0.0.1."""
+    import sys
+    return [python or sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={int(nproc)}", "--master-addr=127.0.0.1",
+            f"--master-port={int(port or free_port())}", script, *argv]
+
+
+def maybe_self_launch(script, argv, nproc, env=None):
+    """bench.py --gpus N run without torchrun: spawn the N ranks here and
+    return their exit code; None when already inside a launched job (or N=1)."""
+    import os
+    import subprocess
+    env = os.environ if env is None else env
+    if nproc <= 1 or "WORLD_SIZE" in env:
+        return None
+    return subprocess.call(torchrun_argv(script, argv, nproc), env=dict(env))
