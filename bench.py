@@ -281,6 +281,62 @@ def measured_peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def pipe_peaks():
+    """Measured per-pipe peaks of this B200 (scripts/probes/pipe_peaks.cu,
+    profiles/peaks_fp64_int.json) plus the HBM copy peak, in G op/s (GB/s)."""
+    hbm, hbm_src = measured_peak_hbm()
+    pk = {"hbm": (hbm, hbm_src)}
+    try:
+        j = json.load(open(os.path.join(ROOT, "profiles", "peaks_fp64_int.json")))["peaks"]
+        src = "measured (profiles/peaks_fp64_int.json, scripts/probes/pipe_peaks.cu)"
+        pk["fp64"] = (j["dadd"]["Gop_s"], src)
+        pk["fp64_div"] = (j["ddiv_rn"]["Gop_s"], src)
+        pk["fp32"] = (j["ffma"]["Gop_s"], src)
+        pk["popc"] = (j["popc"]["Gop_s"], src)
+    except Exception:  # B200_PROFILING.md-style nominal fallbacks at 1965 MHz, 148 SMs
+        f = 148 * 1.965
+        src = "fallback (nominal per-SM rates x 148 SMs x 1965 MHz)"
+        pk.update({"fp64": (64 * f, src), "fp64_div": (4 * f, src), "fp32": (128 * f, src),
+                   "popc": (16 * f, src)})
+    return pk
+
+
+def kernel_roofline(lib, rig, key, avg_ms, launches):
+    """One kernel against every pipe its algorithmic work uses; the bound is
+    the pipe with the largest fraction of its peak. FP64 divisions/square
+    roots are converted to add/mul slots by the measured peak ratio, so the
+    FP64 figure is 'DADD-equivalent G op/s' against the DADD peak. Peaks of a
+    launch that can occupy only some SMs (one cluster per camera pair) are
+    scaled to those SMs."""
+    w = (C.c_double * 6)()
+    st = lib.lp_rig_algorithmic_work(rig, key.encode(), int(launches), w)
+    pk = pipe_peaks()
+    t = avg_ms * 1e-3
+    occ = (w[5] / 148.0) if w[5] > 0 else 1.0
+    pipes = {}
+    if st == 0 and w[0] > 0:
+        pipes["hbm"] = (w[0] / 1e9, pk["hbm"][0], "GB/s", pk["hbm"][1])
+    if st == 0 and (w[1] > 0 or w[2] > 0):
+        eq = w[1] + w[2] * pk["fp64"][0] / pk["fp64_div"][0]
+        pipes["fp64"] = (eq / 1e9, pk["fp64"][0] * occ, "Gop/s (DADD-equivalent)", pk["fp64"][1])
+    if st == 0 and w[3] > 0:
+        pipes["fp32"] = (w[3] / 1e9, pk["fp32"][0] * occ, "Gop/s", pk["fp32"][1])
+    if st == 0 and w[4] > 0:
+        pipes["popc"] = (w[4] / 1e9, pk["popc"][0] * occ, "Gop/s", pk["popc"][1])
+    if not pipes:
+        return {"bound": None, "achieved": None, "peak": None, "unit": None, "frac": None,
+                "avg_launch_ms": avg_ms, "algorithmic": None}
+    fr = {p: (v[0] / t) / v[1] for p, v in pipes.items()}
+    b = max(fr, key=fr.get)
+    g, peak, unit, src = pipes[b]
+    return {"bound": b, "achieved": g / t, "peak": peak, "unit": unit, "frac": fr[b],
+            "peak_source": src + (f", scaled to the {int(w[5])} SMs the launch occupies" if w[5] > 0 else ""),
+            "avg_launch_ms": avg_ms,
+            "algorithmic": {"bytes": w[0], "fp64_addmul_ops": w[1], "fp64_div_sqrt_ops": w[2],
+                            "fp32_ops": w[3], "popc_ops": w[4]},
+            "frac_by_pipe": {p: round(f, 4) for p, f in fr.items()}}
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -526,6 +582,7 @@ def main():
         # concurrent extraction does not inflate the compositor's kernels
         lib.lp_rig_set_streams(rig.rig, 1)
         lib.lp_profile_reset()
+        lib.lp_rig_work_reset(rig.rig)
         lib.lp_profile_enable(1)
         for i in range(args.steps):
             step(10_000 + i)
@@ -542,14 +599,14 @@ def main():
         for i in range(min(n, cap)):
             key = names.raw[i * 64:(i + 1) * 64].split(b"\0")[0].decode()
             kern[key] = (tot[i], cnt[i])
-        lib.lp_rig_algorithmic_bytes.argtypes = [C.c_void_p, C.c_char_p]
-        lib.lp_rig_algorithmic_bytes.restype = C.c_double
         step_ms = sum(v[0] for v in kern.values()) / args.steps
         dom = max(kern, key=lambda k: kern[k][0])
-        avg = kern[dom][0] / kern[dom][1]
-        byts = lib.lp_rig_algorithmic_bytes(rig.rig, dom.encode())
-        peak, peak_src = measured_peak_hbm()
-        achieved = byts / (avg * 1e-3) / 1e9 if byts > 0 else None
+        # every kernel against the pipe its exact arithmetic needs most of
+        # (lp_rig_algorithmic_work: compulsory bytes, FP64 add/mul/compare,
+        # FP64 div/sqrt, FP32, POPC); the bound is the pipe with the largest
+        # fraction of its measured peak
+        per_kernel = {k: kernel_roofline(lib, rig.rig, k, kern[k][0] / kern[k][1], kern[k][1])
+                      for k in kern}
         # DRAM bytes of the same launch from the committed ncu --set full capture
         # (scripts/ncu_traffic.py -> profiles/ncu_traffic.json), or null
         traffic, limiter = None, None
@@ -559,13 +616,14 @@ def main():
             limiter = nj.get(args.config, {}).get(dom, {}).get("limiter")
         except Exception:
             pass
-        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                    "peak_source": peak_src, "unit": "GB/s",
-                    "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                    "algorithmic_bytes_per_launch": byts, "avg_launch_ms": avg,
-                    # what does bound it (same ncu capture): issue slots / FP64 pipe / DRAM
-                    "ncu_limiter": limiter,
-                    "share_of_kernel_time": kern[dom][0] / max(1e-9, sum(v[0] for v in kern.values()))}
+        roofline = dict(per_kernel[dom])
+        roofline.update({"kernel": dom, "traffic": traffic,
+                         # what ncu says bounds it (same capture): issue slots / FP64 pipe / DRAM
+                         "ncu_limiter": limiter,
+                         "share_of_kernel_time": kern[dom][0] / max(1e-9, sum(v[0] for v in kern.values())),
+                         "kernels": {k: {"ms": round(v["avg_launch_ms"], 4), "bound": v["bound"],
+                                         "frac": None if v["frac"] is None else round(v["frac"], 4)}
+                                     for k, v in sorted(per_kernel.items(), key=lambda kv: -kern[kv[0]][0])}})
         stage = {k: round(v[0] / v[1], 4) for k, v in sorted(kern.items(), key=lambda kv: -kv[1][0])}
         stage["_kernel_ms_per_frame"] = round(step_ms, 4)
         # the reference's stages (pipeline.hpp:26-34), device ms per frame

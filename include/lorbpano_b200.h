@@ -182,6 +182,11 @@ lp_status lp_match_features(lp_ctx* ctx, const uint64_t* set_a, int na, const ui
 
 /* dlt_homography, homography.hpp:114-144 */
 lp_status lp_dlt_homography(lp_ctx* ctx, const lp_corr* pairs, int n, lp_homography* out);
+/* symmetric_transfer_error (homography.hpp:147-152) of each of n pairs:
+ * |H(s) - d| + |H^-1(d) - s| with glibc's hypot, bit-identical to the
+ * reference's std::hypot. */
+lp_status lp_symmetric_transfer_errors(lp_ctx* ctx, const lp_homography* h, const lp_homography* h_inv,
+                                       const lp_corr* pairs, int n, double* out);
 /* prosac_homography, homography.hpp:182-286. trace_* optional (NULL), sized
  * max_iter and 4*max_iter; *iterations gives the filled length. */
 lp_status lp_prosac_homography(lp_ctx* ctx, const lp_corr* matches, int n,
@@ -289,6 +294,13 @@ lp_status lp_rig_stitch(lp_rig* rig, const uint8_t* const* images, uint64_t fram
  * one launch of `kernel_key` ("k_warp/0", "k_blend_level/3", ... as the
  * profiler names them) moves for the rig's last frame; < 0 if unknown. */
 double lp_rig_algorithmic_bytes(lp_rig* rig, const char* kernel_key);
+/* Algorithmic work of one launch of `kernel_key` by pipe, for the roofline:
+ * out6[0] compulsory bytes, [1] FP64 add/mul/compare ops, [2] FP64
+ * divisions + square roots, [3] FP32 ops, [4] 32-bit POPC ops, [5] SMs the
+ * launch can occupy (0 = all). Launch-varying counts (Harris candidates) are
+ * averaged over `launches` launches since lp_rig_work_reset. Profiling only. */
+lp_status lp_rig_algorithmic_work(lp_rig* rig, const char* kernel_key, long long launches, double* out6);
+lp_status lp_rig_work_reset(lp_rig* rig);
 
 /* Failure injection (tests of the per-frame failure path): the frame
  * submitted with `frame_index` raises device status `code` on its slot, as a

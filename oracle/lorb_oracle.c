@@ -915,6 +915,12 @@ static double ste(const double* h, const double* hi, const lp_corr* c) {
     return hypot(fx - c->dx, fy - c->dy) + hypot(bx - c->sx, by - c->sy);
 }
 
+int orc_symmetric_transfer_errors(const lp_homography* h, const lp_homography* hi, const lp_corr* c, int n,
+                                  double* out) {
+    for (int i = 0; i < n; ++i) out[i] = ste(h->h, hi->h, c + i);
+    return LP_OK;
+}
+
 /* prosac_homography, homography.hpp:182-286 */
 int orc_prosac_homography(const lp_corr* m, int n, const lp_prosac_config* cfg,
                           lp_homography* model, uint8_t* mask_out, int* inlier_count,

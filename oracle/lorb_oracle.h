@@ -34,6 +34,8 @@ int orc_probe_sequence(int k, int t, uint64_t* out);
 int orc_match_features(const uint64_t* a, int na, const uint64_t* b, int nb, int n_d,
                        const lp_match_config* cfg, lp_match* out, int cap, int* count);
 int orc_dlt_homography(const lp_corr* c, int n, lp_homography* out);
+int orc_symmetric_transfer_errors(const lp_homography* h, const lp_homography* hi, const lp_corr* c, int n,
+                                  double* out);
 int orc_prosac_homography(const lp_corr* c, int n, const lp_prosac_config* cfg,
                           lp_homography* model, uint8_t* mask, int* inlier_count, int* iterations,
                           int* trace_pool, int* trace_samples);

@@ -379,6 +379,18 @@ int ref_dlt_homography(const lp_corr* c, int n, lp_homography* out) {
         for (int i = 0; i < 9; ++i) out->h[i] = h.h[i];
     });
 }
+int ref_symmetric_transfer_errors(const lp_homography* h, const lp_homography* hi, const lp_corr* c, int n,
+                                  double* out) {
+    return guard([&] {
+        Homography a, b;
+        for (int i = 0; i < 9; ++i) {
+            a.h[i] = h->h[i];
+            b.h[i] = hi->h[i];
+        }
+        auto v = corrs(c, n);
+        for (int i = 0; i < n; ++i) out[i] = symmetric_transfer_error(a, b, v[i]);
+    });
+}
 int ref_prosac_homography(const lp_corr* c, int n, const lp_prosac_config* cfg, lp_homography* model,
                           std::uint8_t* mask, int* inlier_count, int* iterations, int* trace_pool,
                           int* trace_samples) {

@@ -214,6 +214,16 @@ class AbiWrapper:
         self._call("dlt_homography", _ptr(corr), len(corr), C.byref(h))
         return np.array(h.h[:], np.float64).reshape(3, 3)
 
+    def symmetric_transfer_errors(self, h, h_inv, corr):
+        """symmetric_transfer_error (homography.hpp:147-152) of every pair."""
+        n = len(corr)
+        out = np.zeros(max(n, 1), np.float64)
+        a, b = abi.Homography(), abi.Homography()
+        a.h[:] = [float(v) for v in np.asarray(h, np.float64).ravel()]
+        b.h[:] = [float(v) for v in np.asarray(h_inv, np.float64).ravel()]
+        self._call("symmetric_transfer_errors", C.byref(a), C.byref(b), _ptr(corr), n, _ptr(out))
+        return out[:n]
+
     def prosac_homography(self, corr, cfg, trace=False):
         n = len(corr)
         h = abi.Homography()

@@ -878,6 +878,20 @@ lp_status lp_dlt_homography(lp_ctx* ctx, const lp_corr* pairs, int n, lp_homogra
     });
 }
 
+lp_status lp_symmetric_transfer_errors(lp_ctx* ctx, const lp_homography* h, const lp_homography* h_inv,
+                                       const lp_corr* pairs, int n, double* out) {
+    return guard([&] {
+        if (n < 0) throw Status(LP_BAD_PARAMS, "symmetric_transfer_error: n < 0");
+        if (n == 0) return;
+        cudaStream_t s = ctx->stream;
+        In<lp_corr> dc(pairs, n, s);
+        Out<double> o(out, n, s);
+        ste_launch(*h, *h_inv, dc.d, n, o.d, s);
+        o.finish(s, n);
+        LPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 lp_status lp_prosac_homography(lp_ctx* ctx, const lp_corr* matches, int n, const lp_prosac_config* cfg,
                                lp_homography* model, uint8_t* mask, int* inlier_count, int* iterations,
                                int* trace_pool, int* trace_samples) {

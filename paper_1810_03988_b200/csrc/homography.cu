@@ -20,6 +20,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "homography.cuh"
+#include <math_constants.h>
 
 namespace lpb {
 
@@ -164,11 +165,56 @@ __device__ bool h_inverse(const double* h, double* out) {
         for (int i = 0; i < 9; ++i) out[i] /= inv[8];
     return true;
 }
+// std::hypot as glibc >= 2.35 computes it on x86-64 (the reference's libm;
+// no FMA in that build): order the magnitudes, the EPS / LARGE / TINY
+// shortcuts with 2^-600 scaling, then h = sqrt(ax^2 + ay^2) corrected by one
+// exact-residual Newton step (Borges, "An improved algorithm for hypot(a, b)",
+// the non-FMA variant). CUDA's hypot is not that function and can differ in
+// the last ulp, which could move an error across the inlier threshold or
+// flip an equal-count error-sum tie (homography.hpp:206-221); this one is
+// bit-identical to the host's (tests/test_gpu_parity.py: ste bit parity, and
+// oracle/hypot_check.c against libm on 5e7 inputs). --fmad=false keeps every
+// product and sum below separately rounded, as in the x86 build.
+__device__ __forceinline__ double glibc_hypot_kernel(double ax, double ay) {
+    double h = sqrt(ax * ax + ay * ay);
+    double t1, t2;
+    if (h <= 2.0 * ay) {
+        const double delta = h - ay;
+        t1 = ax * (2.0 * delta - ax);
+        t2 = (delta - 2.0 * (ax - ay)) * delta;
+    } else {
+        const double delta = h - ax;
+        t1 = 2.0 * delta * (ax - 2.0 * ay);
+        t2 = (4.0 * delta - ay) * ay + delta * delta;
+    }
+    h -= (t1 + t2) / (2.0 * h);
+    return h;
+}
+__device__ double glibc_hypot(double x, double y) {
+    if (!isfinite(x) || !isfinite(y)) {
+        if (isinf(x) || isinf(y)) return CUDART_INF;
+        return x + y;  // NaN
+    }
+    x = fabs(x);
+    y = fabs(y);
+    const double ax = x < y ? y : x, ay = x < y ? x : y;
+    constexpr double kScale = 0x1p-600, kLarge = 0x1p+511, kTiny = 0x1p-511, kEps = 0x1p-54;
+    if (ax > kLarge) {
+        if (ay <= ax * kEps) return ax + ay;
+        return glibc_hypot_kernel(ax * kScale, ay * kScale) / kScale;
+    }
+    if (ay < kTiny) {
+        if (ax >= ay / kEps) return ax + ay;
+        return glibc_hypot_kernel(ax / kScale, ay / kScale) * kScale;
+    }
+    if (ay <= ax * kEps) return ax + ay;
+    return glibc_hypot_kernel(ax, ay);
+}
 __device__ __forceinline__ double ste(const double* h, const double* hi, const lp_corr& c) {
     double fx, fy, bx, by;
     h_apply(h, c.sx, c.sy, fx, fy);
     h_apply(hi, c.dx, c.dy, bx, by);
-    return hypot(fx - c.dx, fy - c.dy) + hypot(bx - c.sx, by - c.sy);
+    return glibc_hypot(fx - c.dx, fy - c.dy) + glibc_hypot(bx - c.sx, by - c.sy);
 }
 
 struct Norm {
@@ -626,7 +672,7 @@ __device__ int block_compact(int n, int* idx, F flag) {
     return base;
 }
 
-constexpr int kChunk = 8;  // hypotheses per round = warps per CTA (or CTAs per cluster)
+constexpr int kChunk = kProsacClusterCtas;  // hypotheses per round = warps per CTA (or CTAs per cluster)
 __device__ __forceinline__ double* s_dyn_refit() {
     extern __shared__ __align__(16) double s_dyn[];
     return s_dyn;
@@ -1085,6 +1131,16 @@ __global__ void __launch_bounds__(256) k_dlt(const lp_corr* c, int n, double* sc
 void dlt_launch(const lp_corr* c, int n, double* scratch, lp_homography* out, int* status,
                 cudaStream_t s) {
     LPB_LAUNCH(k_dlt, 1, 256, 0, s, c, n, scratch, out, status);
+}
+
+// symmetric_transfer_error (homography.hpp:147-152) of n correspondences
+__global__ void k_ste(lp_homography h, lp_homography hi, const lp_corr* c, int n, double* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = ste(h.h, hi.h, c[i]);
+}
+void ste_launch(const lp_homography& h, const lp_homography& hi, const lp_corr* c, int n, double* out,
+                cudaStream_t s) {
+    if (n > 0) LPB_LAUNCH(k_ste, cdiv(n, 256), 256, 0, s, h, hi, c, n, out);
 }
 
 }  // namespace lpb

@@ -34,6 +34,7 @@ struct ProsacArgs {
     unsigned* chain_counter;
 };
 
+constexpr int kProsacClusterCtas = 8;  // k_prosac: CTAs per pair (one thread-block cluster)
 constexpr int kRefitSmemRows = 800;  // 800 x 232 B = 186 KB of dynamic shared memory
 
 // scratch doubles per pair: refit system A (2cap x 9), Householder vector
@@ -48,6 +49,9 @@ void chain_launch(const lp_homography* pair_h, const int* pair_status, int npair
                   lp_homography* chain, int* chain_status, cudaStream_t s);
 
 // dlt_homography on one correspondence set (C-ABI lp_dlt_homography)
+// symmetric_transfer_error of each correspondence (glibc hypot, bit-exact)
+void ste_launch(const lp_homography& h, const lp_homography& hi, const lp_corr* c, int n, double* out,
+                cudaStream_t s);
 void dlt_launch(const lp_corr* c, int n, double* scratch, lp_homography* out, int* status,
                 cudaStream_t s);
 

@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(256, 4) k_detect9(const __grid_constant__ Extr
     __shared__ int s_grad[GY * GX];  // (gx & 0xffff) | gy << 16
     __shared__ float s_resp[NX * NY];
     __shared__ short s_cand[NX * NY];
-    __shared__ int s_ncand;
+    __shared__ int s_ncand, s_ninner;
 
     const int ri = blockIdx.y;
     const DevRegion rg = a.regions[ri];
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(256, 4) k_detect9(const __grid_constant__ Extr
     const int fx0 = (ox - 1) & ~3;  // first FAST word (ox >= 3)
     const int gx0 = fx0 - 4, gy0 = oy - 5;
     const int tid = threadIdx.x, lane = tid & 31;
-    if (tid == 0) s_ncand = 0;
+    if (tid == 0) s_ncand = s_ninner = 0;
 
     // ---- stage: SH rows x SWW words
     const bool inside = gx0 >= 0 && gy0 >= 0 && gx0 + SB <= im.w && gy0 + SH <= im.h && (im.w & 3) == 0 &&
@@ -385,9 +385,11 @@ __global__ void __launch_bounds__(256, 4) k_detect9(const __grid_constant__ Extr
     // ---- FP64 Harris over the candidates (lorb.hpp:235-247), exact x4 scaled
     const int nc = s_ncand;
     const double alpha = static_cast<double>(a.alpha);
+    int ninner = 0;  // the tile's own candidates (the ring belongs to its neighbours)
     for (int jj = tid; jj < nc; jj += 256) {
         const int i = s_cand[jj];
         const int ly = i / NX, lx = i - ly * NX;
+        ninner += lx >= 1 && lx <= TX && ly >= 1 && ly <= TY;
         const int* g0 = s_grad + ly * GX + lx;  // tap (u, v) = (-3, -3)
         double sa = 0.0, sb = 0.0, sc = 0.0;
 #pragma unroll
@@ -411,7 +413,12 @@ __global__ void __launch_bounds__(256, 4) k_detect9(const __grid_constant__ Extr
         const float rf = __double2float_rn(r);
         if (rf >= a.threshold) s_resp[i] = rf;
     }
+    if (a.work_cand) {  // Harris evaluations, for the roofline (lp_rig_algorithmic_work)
+        ninner = __reduce_add_sync(0xffffffffu, ninner);
+        if (lane == 0 && ninner) atomicAdd(&s_ninner, ninner);
+    }
     __syncthreads();
+    if (a.work_cand && tid == 0 && s_ninner) atomicAdd(a.work_cand, static_cast<unsigned long long>(s_ninner));
 
     // ---- 3x3 NMS over the tile's candidates; survivors -> key list
     for (int b0 = 0; b0 < nc; b0 += 256) {

@@ -57,6 +57,9 @@ struct ExtractArgs {
     uint64_t* lsh_keys;
     const int* lsh_bitpos;   // tables * bits
     int lsh_tables, lsh_bits;
+    // optional (k_detect9): running count of FAST candidates whose FP64 Harris
+    // response was evaluated (each tile's own pixels), for the roofline
+    unsigned long long* work_cand;
 };
 
 // stage_detect + stage_describe for every region of every image in 4 launches

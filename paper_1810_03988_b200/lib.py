@@ -87,6 +87,10 @@ def load():
         lib.lp_rig_inject_fault.restype = C.c_int
         lib.lp_rig_algorithmic_bytes.argtypes = [P, C.c_char_p]
         lib.lp_rig_algorithmic_bytes.restype = C.c_double
+        lib.lp_rig_algorithmic_work.argtypes = [P, C.c_char_p, C.c_longlong, C.POINTER(C.c_double)]
+        lib.lp_rig_algorithmic_work.restype = C.c_int
+        lib.lp_rig_work_reset.argtypes = [P]
+        lib.lp_rig_work_reset.restype = C.c_int
         lib.lp_profile_enable.argtypes = [C.c_int]
         lib.lp_profile_enable.restype = None
         lib.lp_profile_reset.argtypes = []

@@ -1,31 +1,51 @@
 #!/usr/bin/env python
-"""Summarise an `ncu --page source --csv --print-source sass` export: total
-executed warp instructions, per-opcode counts and the hottest instructions
-(by stall samples)."""
-import collections
+"""Summarise one kernel block of an `ncu --page source --csv --print-source sass`
+export: instruction mix by opcode and the hottest instructions by warp
+instructions executed and by stall samples.
+usage: sass_hot.py FILE BLOCK_INDEX [TOP]"""
 import csv
 import sys
+from collections import Counter
 
-rows = list(csv.reader(open(sys.argv[1])))
-hdr = rows[1]
-ix = {n: i for i, n in enumerate(hdr)}
-body = [r for r in rows[2:] if len(r) == len(hdr)]
-def num(r, k):
-    try:
-        return float(r[ix[k]] or 0)
-    except (ValueError, KeyError):
-        return 0.0
-tot = sum(num(r, "Instructions Executed") for r in body)
-samp = sum(num(r, "Warp Stall Sampling (All Samples)") for r in body)
-print(f"{rows[0][1]}: {len(body)} SASS lines, {tot:.4g} warp inst, {samp:.0f} stall samples")
-ops = collections.Counter()
-for r in body:
-    op = r[ix["Source"]].split()[0] if r[ix["Source"]].split() else "?"
-    if op.startswith("@"):
-        op = r[ix["Source"]].split()[1]
-    ops[op.split(".")[0]] += num(r, "Instructions Executed")
-print("opcodes:", ", ".join(f"{k} {v / tot:.1%}" for k, v in ops.most_common(18)))
-n = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-for r in sorted(body, key=lambda r: -num(r, "Warp Stall Sampling (All Samples)"))[:n]:
-    print(f"{r[ix['Address']]:>6} {num(r, 'Warp Stall Sampling (All Samples)'):6.0f} "
-          f"{num(r, 'Instructions Executed'):10.0f}  {r[ix['Source']][:90]}")
+
+def blocks(path):
+    cur, hdr, name = None, None, None
+    for row in csv.reader(open(path)):
+        if row and row[0] == "Kernel Name":
+            if cur is not None:
+                yield name, hdr, cur
+            name, cur, hdr = row[1], [], None
+        elif hdr is None:
+            hdr = row
+        else:
+            cur.append(row)
+    if cur is not None:
+        yield name, hdr, cur
+
+
+def main(path, bi, top=25):
+    for i, (name, hdr, rows) in enumerate(blocks(path)):
+        if i != bi:
+            continue
+        ix = {h: j for j, h in enumerate(hdr)}
+        ie, iss = ix["Instructions Executed"], ix["Warp Stall Sampling (All Samples)"]
+        tot = sum(float(r[ie] or 0) for r in rows)
+        stot = sum(float(r[iss] or 0) for r in rows)
+        print(f"{name}: {tot / 1e6:.2f} M warp instructions, {stot:.0f} stall samples")
+        mix = Counter()
+        for r in rows:
+            op = r[ix["Source"]].split()[0] if r[ix["Source"]].split() else "?"
+            if op.startswith("@"):
+                op = r[ix["Source"]].split()[1]
+            mix[op.split(".")[0]] += float(r[ie] or 0)
+        print("mix:", ", ".join(f"{k} {v / tot * 100:.1f}%" for k, v in mix.most_common(18)))
+        print("-- by executed")
+        for r in sorted(rows, key=lambda r: -float(r[ie] or 0))[:top]:
+            print(f"{r[ix['Address']]:>6} {float(r[ie] or 0) / 1e3:9.1f}K {float(r[iss] or 0):7.0f}  {r[ix['Source']][:90]}")
+        print("-- by stall samples")
+        for r in sorted(rows, key=lambda r: -float(r[iss] or 0))[:top]:
+            print(f"{r[ix['Address']]:>6} {float(r[ie] or 0) / 1e3:9.1f}K {float(r[iss] or 0):7.0f}  {r[ix['Source']][:90]}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], int(sys.argv[2]), int(sys.argv[3]) if len(sys.argv) > 3 else 25)
