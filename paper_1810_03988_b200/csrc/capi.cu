@@ -1132,6 +1132,7 @@ struct ComposeBuffers {
 
     DBuf runs, runs_used, status;
     std::vector<float*> host_G, host_M;  // [c * levels + k]
+    std::vector<PyrTma> pyr_tma;         // per source level k: k_pyr_down2's tensor maps
 
     // analytic: level-0 masks come from coverage runs (the rig); otherwise the
     // caller fills M[c][0] (lp_multiband_blend).
@@ -1206,6 +1207,24 @@ struct ComposeBuffers {
         args.status = status.as<int>();
         auto taps = host::gaussian_kernel(1.0f);
         for (int q = 0; q < 7; ++q) args.down_taps[q] = taps[q];
+        // TMA staging of the pyramid boxes (LPB_TMA=0: cp.async everywhere)
+        pyr_tma.assign(std::max(levels - 1, 1), PyrTma{});
+        args.pyr_tma = nullptr;
+        const char* env = std::getenv("LPB_TMA");
+        if (levels > 1 && !(env && env[0] == '0')) {
+            bool ok = true;
+            for (int k = 0; k + 1 < levels && ok; ++k) {
+                PyrTma& t = pyr_tma[k];
+                for (int c = 0; c < ncams && ok; ++c) {
+                    const Win& w = win[c * levels + k];
+                    if (w.w == 0 || w.h == 0) continue;  // no CTA of this camera stages at level k
+                    ok = tma_encode_f32_2d(&t.g[c], args.G[c][k], w.w, w.h, w.p, PD2_BW, PD2_BH) &&
+                         tma_encode_f32_2d(&t.m[c], args.M[c][k], w.w, w.h, w.p, PD2_BW, PD2_BH);
+                }
+                t.ok = 1;
+            }
+            if (ok) args.pyr_tma = pyr_tma.data();
+        }
     }
 };
 

@@ -1,5 +1,7 @@
 // compose.cuh — warp + seam + multi-band blend on the device (compose.hpp:32-215).
 #pragma once
+#include <cuda.h>  // CUtensorMap
+
 #include "common.cuh"
 
 namespace lpb {
@@ -15,6 +17,23 @@ constexpr int kMaxCompCams = 16;   // cameras per rig on the fused compositor pa
 constexpr int kMaxCompLevels = 12; // blend levels (canvas >= 2^11 px per side for 12)
 constexpr int kRunSlots = 4;       // coverage runs stored inline per window row
 constexpr int kBlendAlignX = 64;   // level-0 window x alignment (blend tile width at level 0)
+
+// k_pyr_down output tile (level k+1) and its staged level-k box
+constexpr int PD2_TX = 64, PD2_TY = 16;
+constexpr int PD2_BW = 2 * PD2_TX + 8, PD2_BH = 2 * PD2_TY + 6;  // box 136 x 38 (134 used; rows of 16 B)
+
+// Tensor maps of one k_pyr_down2 launch (level k -> k+1): every camera's
+// level-k image and mask window as a 2-D f32 tensor (window-local
+// coordinates, pitch w.p), box PD2_BW x PD2_BH. Passed by value as a
+// __grid_constant__ parameter; ok == 0 -> the cp.async staging path.
+struct PyrTma {
+    CUtensorMap g[kMaxCompCams], m[kMaxCompCams];
+    int ok;
+};
+
+// Encode a 2-D f32 tensor map (w x h elements, row pitch `pitch` elements,
+// box bw x bh, zero fill out of bounds). False if the driver refuses.
+bool tma_encode_f32_2d(CUtensorMap* m, const float* base, int w, int h, int pitch, int bw, int bh);
 
 // Passed by value (constant bank): all per-camera geometry and pointers.
 struct ComposeArgs {
@@ -41,11 +60,10 @@ struct ComposeArgs {
     double hinv[kMaxCompCams][9];
     uint8_t* out;                              // W[0] x H[0]
     int* status;
+    // host pointer (never read on the device): PyrTma per source level k,
+    // owned by the ComposeBuffers that built this geometry, or null
+    const PyrTma* pyr_tma;
 };
-
-// k_pyr_down output tile (level k+1) and its staged level-k box
-constexpr int PD2_TX = 64, PD2_TY = 16;
-constexpr int PD2_BW = 2 * PD2_TX + 8, PD2_BH = 2 * PD2_TY + 6;  // box 136 x 38 (134 used; rows of 16 B)
 
 // stage_rectify_crop (pipeline.hpp:391-417) of one camera: dst (w x h, the
 // crop's size) from src (in_w x in_h)

@@ -296,6 +296,26 @@ def test_stitch_chain_4cam_small(lp, orc, params):
                         orc.stitch_frame(cams, params, frame_index=2))
 
 
+def test_pyramid_tma_staging_matches_cp_async(lp, orc, params, monkeypatch):
+    """k_pyr_down2 stages interior boxes with TMA tensor loads (zero fill
+    outside the camera window) and canvas-edge boxes with cp.async; with
+    LPB_TMA=0 every box takes the cp.async path. Both panoramas must equal the
+    oracle's bit for bit (1920x1080 x 4 chain: 5 pyramid levels' worth of
+    interior and edge boxes)."""
+    from paper_1810_03988_b200 import Rig
+    p = orc.default_params()
+    p.seed = p.matching.seed = 42
+    cams, wide, shift = chain_cameras(orc, 4, 1920, 1080)
+    want = orc.stitch_frame(cams, p, frame_index=0)
+    got = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("LPB_TMA", mode)
+        rig = Rig(lp, 4, 1920, 1080, p)
+        got[mode] = rig.stitch(cams, 0)["panorama"]
+    assert np.array_equal(got["1"], want["panorama"])
+    assert np.array_equal(got["0"], want["panorama"])
+
+
 def test_rig_cache_and_device_inputs(lp, orc, params):
     """HomographyCache semantics (pipeline.hpp:259-286) and device-resident inputs."""
     import torch
