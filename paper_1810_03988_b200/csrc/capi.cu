@@ -1133,6 +1133,7 @@ struct ComposeBuffers {
     DBuf runs, runs_used, status;
     std::vector<float*> host_G, host_M;  // [c * levels + k]
     std::vector<PyrTma> pyr_tma;         // per source level k: k_pyr_down2's tensor maps
+    std::vector<BlendTma> blend_tma;     // per level k < levels - 1: k_blend_lean's tensor maps
 
     // analytic: level-0 masks come from coverage runs (the rig); otherwise the
     // caller fills M[c][0] (lp_multiband_blend).
@@ -1210,6 +1211,7 @@ struct ComposeBuffers {
         // TMA staging of the pyramid boxes (LPB_TMA=0: cp.async everywhere)
         pyr_tma.assign(std::max(levels - 1, 1), PyrTma{});
         args.pyr_tma = nullptr;
+        args.blend_tma = nullptr;
         const char* env = std::getenv("LPB_TMA");
         if (levels > 1 && !(env && env[0] == '0')) {
             bool ok = true;
@@ -1224,6 +1226,24 @@ struct ComposeBuffers {
                 t.ok = 1;
             }
             if (ok) args.pyr_tma = pyr_tma.data();
+            // k_blend_lean<64 >> k> stages level k+1 of every camera and R_k+1
+            blend_tma.assign(levels - 1, BlendTma{});
+            ok = true;
+            for (int k = 0; k + 1 < levels && ok; ++k) {
+                const int txk = kBlendAlignX >> k;
+                if (txk < 4) break;
+                const int cx = lean_cx(txk), cy = lean_cy(txk);
+                if (cx > 256 || cy > 256) continue;  // beyond the TMA box limit: cp.async
+                BlendTma& t = blend_tma[k];
+                for (int c = 0; c < ncams && ok; ++c) {
+                    const Win& w = win[c * levels + k + 1];
+                    if (w.w == 0 || w.h == 0) continue;
+                    ok = tma_encode_f32_2d(&t.g[c], args.G[c][k + 1], w.w, w.h, w.p, cx, cy);
+                }
+                ok = ok && tma_encode_f32_2d(&t.r, args.R[k + 1], args.W[k + 1], args.H[k + 1], args.Rp[k + 1], cx, cy);
+                t.ok = ok ? 1 : 0;
+            }
+            if (ok) args.blend_tma = blend_tma.data();
         }
     }
 };

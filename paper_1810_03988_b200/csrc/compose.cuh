@@ -31,6 +31,17 @@ struct PyrTma {
     int ok;
 };
 
+// Tensor maps of one k_blend_lean launch at level k (< levels - 1): every
+// camera's level-(k+1) image window and the level-(k+1) collapse result R,
+// box lean_cx(TXK) x lean_cy(TXK); ok == 0 -> cp.async staging.
+struct BlendTma {
+    CUtensorMap g[kMaxCompCams], r;
+    int ok;
+};
+// staged coarse tile of k_blend_lean<TXK>: rows, columns (16-byte rows)
+__host__ __device__ constexpr int lean_cy(int txk) { return 4096 / txk / 2 + 3; }
+__host__ __device__ constexpr int lean_cx(int txk) { return (txk / 2 + 3 + 3 + 3) / 4 * 4; }
+
 // Encode a 2-D f32 tensor map (w x h elements, row pitch `pitch` elements,
 // box bw x bh, zero fill out of bounds). False if the driver refuses.
 bool tma_encode_f32_2d(CUtensorMap* m, const float* base, int w, int h, int pitch, int bw, int bh);
@@ -63,6 +74,7 @@ struct ComposeArgs {
     // host pointer (never read on the device): PyrTma per source level k,
     // owned by the ComposeBuffers that built this geometry, or null
     const PyrTma* pyr_tma;
+    const BlendTma* blend_tma;  // host pointer: BlendTma per level k < levels - 1, or null
 };
 
 // stage_rectify_crop (pipeline.hpp:391-417) of one camera: dst (w x h, the
