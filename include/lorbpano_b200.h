@@ -325,6 +325,16 @@ int lp_profile_read(char* names, int name_stride, double* total_ms, long long* l
 lp_status lp_rig_submit(lp_rig* rig, const uint8_t* const* images, uint64_t frame_index,
                         uint8_t* panorama, size_t pano_cap, uint64_t* ticket);
 lp_status lp_rig_wait(lp_rig* rig, uint64_t ticket, lp_canvas* canvas);
+/* Frames in flight WITH their per-frame results (StitchEngine's FramePacket,
+ * pipeline.hpp:50-65): out->panorama receives the panorama as in
+ * lp_rig_submit; the keypoints / descriptors / matches requested in `out`
+ * are staged per frame slot and, with the canvas, the estimate flag, the
+ * homographies and the device stage times, land in `out` at
+ * lp_rig_wait_frame. `out` must stay valid until then; collect a ticket
+ * before submitting 3 more frames (the slot is reused). */
+lp_status lp_rig_submit_frame(lp_rig* rig, const uint8_t* const* images, uint64_t frame_index, lp_frame_out* out,
+                              uint64_t* ticket);
+lp_status lp_rig_wait_frame(lp_rig* rig, uint64_t ticket, lp_frame_out* out);
 
 /* Egress format of lp_rig_submit / lp_rig_stitch panoramas: 1 = the PPM sink's
  * 3-channel RGB (gray triplicated on the device before the copy out,

@@ -79,6 +79,10 @@ def load():
         lib.lp_rig_submit.restype = C.c_int
         lib.lp_rig_wait.argtypes = [P, C.c_uint64, C.POINTER(abi.Canvas)]
         lib.lp_rig_wait.restype = C.c_int
+        lib.lp_rig_submit_frame.argtypes = [P, P, C.c_uint64, C.POINTER(abi.FrameOut), C.POINTER(C.c_uint64)]
+        lib.lp_rig_submit_frame.restype = C.c_int
+        lib.lp_rig_wait_frame.argtypes = [P, C.c_uint64, C.POINTER(abi.FrameOut)]
+        lib.lp_rig_wait_frame.restype = C.c_int
         lib.lp_rig_set_graphs.argtypes = [P, C.c_int]
         lib.lp_rig_set_graphs.restype = C.c_int
         lib.lp_rig_set_streams.argtypes = [P, C.c_int]
@@ -234,7 +238,8 @@ class Rig:
         arr = (C.c_void_p * self.ncams)(*image_ptrs)
         _check(self.lib, self.lib.lp_rig_stitch(self.rig, arr, frame_index, C.byref(fo)))
 
-    def stitch(self, images, frame_index=0, pano_cap=None, details=False):
+    def _frame_out(self, images, pano_cap, details):
+        """Host buffers + FrameOut for one frame (keeps the arrays alive)."""
         ptrs = []
         keep = []
         for im in images:
@@ -247,43 +252,69 @@ class Rig:
         p = self.params
         ncams = self.ncams
         pano_cap = pano_cap or self.panorama_capacity()
-        pano = np.zeros(pano_cap, np.uint8)
-        homs = (abi.Homography * ncams)()
+        st = dict(ptrs=ptrs, keep=keep, details=details)
+        st["pano"] = np.zeros(pano_cap, np.uint8)
+        st["homs"] = (abi.Homography * ncams)()
         fo = abi.FrameOut()
-        fo.panorama = pano.ctypes.data_as(abi.c_u8p)
+        fo.panorama = st["pano"].ctypes.data_as(abi.c_u8p)
         fo.pano_cap = pano_cap
-        fo.homographies = homs
+        fo.homographies = st["homs"]
         if details:
             cap_kp = 2 * p.extraction.top_n
             W = (p.extraction.n_d + 63) // 64
-            kpc = np.zeros(ncams, np.int32)
-            kps = np.zeros((ncams, cap_kp, 4), np.int32)
-            desc = np.zeros((ncams, cap_kp, 2 * W), np.uint64)
-            mc = np.zeros(max(ncams - 1, 1), np.int32)
-            mt = np.zeros((max(ncams - 1, 1), cap_kp, 4), np.int32)
-            fo.kp_counts = kpc.ctypes.data_as(abi.c_intp)
-            fo.keypoints = kps.ctypes.data_as(C.POINTER(abi.Keypoint))
-            fo.descriptors = desc.ctypes.data_as(abi.c_u64p)
+            st["kpc"] = np.zeros(ncams, np.int32)
+            st["kps"] = np.zeros((ncams, cap_kp, 4), np.int32)
+            st["desc"] = np.zeros((ncams, cap_kp, 2 * W), np.uint64)
+            st["mc"] = np.zeros(max(ncams - 1, 1), np.int32)
+            st["mt"] = np.zeros((max(ncams - 1, 1), cap_kp, 4), np.int32)
+            fo.kp_counts = st["kpc"].ctypes.data_as(abi.c_intp)
+            fo.keypoints = st["kps"].ctypes.data_as(C.POINTER(abi.Keypoint))
+            fo.descriptors = st["desc"].ctypes.data_as(abi.c_u64p)
             fo.cap_kp = cap_kp
-            fo.match_counts = mc.ctypes.data_as(abi.c_intp)
-            fo.matches = mt.ctypes.data_as(C.POINTER(abi.Match))
+            fo.match_counts = st["mc"].ctypes.data_as(abi.c_intp)
+            fo.matches = st["mt"].ctypes.data_as(C.POINTER(abi.Match))
             fo.cap_matches = cap_kp
-        self.stitch_raw(ptrs, frame_index, fo)
+        st["fo"] = fo
+        return st
+
+    def _result(self, st):
+        fo, ncams = st["fo"], self.ncams
         cv = fo.canvas
+        homs = st["homs"]
         out = dict(
             canvas=(cv.width, cv.height, cv.origin_x, cv.origin_y),
-            panorama=pano[:cv.width * cv.height].reshape(cv.height, cv.width).copy(),
+            panorama=st["pano"][:cv.width * cv.height].reshape(cv.height, cv.width).copy(),
             homographies=np.array([homs[i].h[:] for i in range(ncams)]).reshape(ncams, 3, 3),
             estimated=bool(fo.estimated),
             stage_ms=list(fo.stage_ms),
         )
-        if details:
+        if st["details"]:
+            kpc, kps, desc, mc, mt = st["kpc"], st["kps"], st["desc"], st["mc"], st["mt"]
             out.update(
                 keypoints=[kps[c, :kpc[c]].copy() for c in range(ncams)],
                 descriptors=[desc[c, :kpc[c]].copy() for c in range(ncams)],
                 matches=[mt[q, :mc[q]].copy() for q in range(ncams - 1)],
             )
         return out
+
+    def stitch(self, images, frame_index=0, pano_cap=None, details=False):
+        st = self._frame_out(images, pano_cap, details)
+        self.stitch_raw(st["ptrs"], frame_index, st["fo"])
+        return self._result(st)
+
+    def submit_frame(self, images, frame_index, details=True, pano_cap=None):
+        """Frame in flight with its per-frame results (lp_rig_submit_frame);
+        wait_frame(handle) returns them as stitch(details=True) does."""
+        st = self._frame_out(images, pano_cap, details)
+        arr = (C.c_void_p * self.ncams)(*st["ptrs"])
+        t = C.c_uint64()
+        _check(self.lib, self.lib.lp_rig_submit_frame(self.rig, arr, frame_index, C.byref(st["fo"]), C.byref(t)))
+        st["ticket"] = t.value
+        return st
+
+    def wait_frame(self, st):
+        _check(self.lib, self.lib.lp_rig_wait_frame(self.rig, st["ticket"], C.byref(st["fo"])))
+        return self._result(st)
 
 
 def load_pnm(path):

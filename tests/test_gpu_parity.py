@@ -403,6 +403,39 @@ def test_rig_frames_in_flight(lp, orc, params):
         assert np.array_equal(got, want[t]), t
 
 
+def test_rig_frames_in_flight_with_details(lp, orc):
+    """lp_rig_submit_frame / lp_rig_wait_frame: 3 frames in flight, each
+    re-registering (refresh 1, moving square), every frame's keypoints,
+    descriptors, matches, homographies and panorama equal to the synchronous
+    details of the same frame and to the oracle's."""
+    from paper_1810_03988_b200 import Rig
+    p = orc.default_params()
+    p.seed = p.matching.seed = 42
+    p.homography_refresh = 1
+    frames = [orc.sequence_frame(480, 270, t, 0.25, 42) for t in range(7)]
+    rig = Rig(lp, 2, 480, 270, p)
+    inflight, got = [], {}
+    for t, (l, r) in enumerate(frames):
+        inflight.append((t, rig.submit_frame([l, r], t)))
+        if len(inflight) == 3:
+            t0, h = inflight.pop(0)
+            got[t0] = rig.wait_frame(h)
+    for t0, h in inflight:
+        got[t0] = rig.wait_frame(h)
+    for t, (l, r) in enumerate(frames):
+        want = orc.stitch_frame([l, r], p, frame_index=t)
+        g = got[t]
+        assert g["estimated"]
+        assert g["canvas"] == want["canvas"], t
+        for c in range(2):
+            assert np.array_equal(g["keypoints"][c], want["keypoints"][c]), (t, c)
+            assert np.array_equal(g["descriptors"][c], want["descriptors"][c]), (t, c)
+        assert np.array_equal(g["matches"][0], want["matches"][0]), t
+        assert np.array_equal(g["homographies"], want["homographies"]), t
+        assert np.array_equal(g["panorama"], want["panorama"]), t
+        assert g["stage_ms"][3] > 0
+
+
 def test_concurrent_rigs_threads(lp, orc):
     """Independent rigs on one context, driven from host threads (the config-5
     shape): each rig has its own stage stream, so their frames overlap on the

@@ -61,6 +61,10 @@ ACCEPT_REF_EXPECTED = {9, 11}
 
 def _accept(path, tmp_path):
     out = subprocess.run([path], capture_output=True, text=True, cwd=tmp_path, timeout=900)
+    # keep the criteria's detail lines (timings, ratios) as evidence
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", os.path.basename(path) + ".log"), "w") as f:
+        f.write(out.stdout)
     failed = {int(m) for m in re.findall(r"^\[FAIL\]\s+(\d+):", out.stdout, re.M)}
     passed = {int(m) for m in re.findall(r"^\[PASS\]\s+(\d+):", out.stdout, re.M)}
     return passed, failed, out.stdout
