@@ -140,6 +140,12 @@ const char* lp_last_error(void);
 /* number of kernels this process launched through the library so far */
 uint64_t lp_kernel_launches(void);
 
+/* Page-locked host memory (cudaHostAlloc) for frames in flight: inputs and
+ * outputs there move by DMA asynchronously; pageable ones make the copy
+ * synchronous with the host. NULL on failure. */
+void* lp_host_alloc(size_t bytes);
+void lp_host_free(void* p);
+
 /* ---- L-ORB primitives (lorb.hpp) ---- */
 
 /* fast_corners, lorb.hpp:192-205: (x,y) pairs in raster order. */

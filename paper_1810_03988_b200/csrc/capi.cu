@@ -358,6 +358,18 @@ extern "C" {
 const char* lp_last_error(void) { return g_err.c_str(); }
 uint64_t lp_kernel_launches(void) { return g_launches.load(); }
 
+void* lp_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, std::max<size_t>(bytes, 1), cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+void lp_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
 void lp_profile_enable(int on) {
     std::lock_guard<std::mutex> l(g_prof.mu);
     g_prof.on = on != 0;

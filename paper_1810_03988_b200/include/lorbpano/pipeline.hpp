@@ -361,15 +361,16 @@ public:
         // frames on the device at once: the rig has 3 frame slots
         const std::size_t depth =
             cfg_.mode == PipelineMode::Serial ? 1 : static_cast<std::size_t>(std::clamp(cfg_.frames_in_flight, 1, 3));
-        std::deque<std::unique_ptr<Flight>> inflight;
-        std::uint64_t index = 0;
+        std::deque<Flight*> inflight;
+        std::uint64_t index = 0, launched = 0;
         for (;;) {
             std::unique_ptr<FramePacket> pkt = ingest(source, index, m);
             if (!pkt) break;
             note_warmup(index + 1);
             ++index;
-            std::unique_ptr<Flight> f = launch(std::move(pkt), m);
-            if (f) inflight.push_back(std::move(f));
+            Flight& f = flights_[launched++ % flights_.size()];
+            launch(f, std::move(pkt), m);
+            inflight.push_back(&f);
             while (inflight.size() >= depth) {
                 land(*inflight.front(), m, sink);
                 inflight.pop_front();
@@ -515,18 +516,36 @@ public:
     }
 
 private:
-    // A frame on the device: its packet and the rig's result arrays.
+    // Page-locked host staging (lp_host_alloc): frames move to and from the
+    // device by DMA, so the host never blocks on a copy while frames are in flight.
+    struct Pinned {
+        void* p = nullptr;
+        std::size_t n = 0;
+        Pinned() = default;
+        Pinned(const Pinned&) = delete;
+        Pinned& operator=(const Pinned&) = delete;
+        ~Pinned() { lp_host_free(p); }
+        template <class T>
+        T* get(std::size_t count) {
+            const std::size_t bytes = count * sizeof(T);
+            if (bytes > n) {
+                lp_host_free(p);
+                p = lp_host_alloc(bytes);
+                if (!p) throw CapacityOverflow("stitch engine: page-locked host staging unavailable");
+                n = bytes;
+            }
+            return static_cast<T*>(p);
+        }
+    };
+
+    // A frame on the device: its packet and the rig's result arrays (one of
+    // three reusable slots, as the rig has three frame slots).
     struct Flight {
         std::unique_ptr<FramePacket> pkt;
         std::uint64_t ticket = 0;
         std::int64_t t_submit = 0;
         lp_frame_out out{};
-        std::vector<lp_homography> homs;
-        std::vector<int> kp_counts, match_counts;
-        std::vector<lp_keypoint> kps;
-        std::vector<std::uint64_t> desc;
-        std::vector<lp_match> matches;
-        std::vector<std::uint8_t> pano;
+        Pinned frames, pano, homs, counts, kps, desc, matches;
     };
 
     int levels_for(int w, int h) const {
@@ -708,8 +727,10 @@ private:
 
     // rectify/crop + regions on the host-visible path, then the frame to the
     // device rig; a frame the rig cannot take runs the stage bodies here
-    std::unique_ptr<Flight> launch(std::unique_ptr<FramePacket> pkt, Metrics& m) {
+    void launch(Flight& f, std::unique_ptr<FramePacket> pkt, Metrics& m) {
         FramePacket& p = *pkt;
+        f.pkt = std::move(pkt);
+        f.ticket = 0;
         const bool rectified = timed_stage(p, Stage::RectifyCrop, m, [&] {
             if (layout_is_identity()) {
                 std::vector<std::pair<int, int>> dims;
@@ -719,49 +740,46 @@ private:
                 stage_rectify_crop(p);
             }
         });
-        if (!rectified || !rig_fits(p)) {
-            if (rectified) run_stage_bodies(p, m);
-            auto f = std::make_unique<Flight>();
-            f->pkt = std::move(pkt);
-            return f;
+        if (!rectified) return;
+        if (!rig_fits(p)) {
+            run_stage_bodies(p, m);
+            return;
         }
         const int ncams = static_cast<int>(p.images.size()), w = p.images[0].width, h = p.images[0].height;
-        auto f = std::make_unique<Flight>();
         try {
             ensure_rig(ncams, w, h);
             const int cap_kp = 2 * params_.extraction.top_n, W2 = 2 * Descriptor::words(params_.extraction.n_d);
-            f->homs.resize(ncams);
-            f->kp_counts.assign(ncams, 0);
-            f->match_counts.assign(std::max(ncams - 1, 1), 0);
-            f->kps.resize(static_cast<std::size_t>(ncams) * cap_kp);
-            f->desc.resize(static_cast<std::size_t>(ncams) * cap_kp * W2);
-            f->matches.resize(static_cast<std::size_t>(std::max(ncams - 1, 1)) * cap_kp);
-            f->pano.resize(lp_rig_panorama_capacity(rig_));
-            lp_frame_out& o = f->out;
-            o.panorama = f->pano.data();
-            o.pano_cap = f->pano.size();
-            o.homographies = f->homs.data();
-            o.kp_counts = f->kp_counts.data();
-            o.keypoints = f->kps.data();
-            o.descriptors = f->desc.data();
+            const std::size_t np = static_cast<std::size_t>(std::max(ncams - 1, 1));
+            const std::size_t fb = static_cast<std::size_t>(w) * h;
+            lp_frame_out& o = f.out;
+            o = lp_frame_out{};
+            o.pano_cap = lp_rig_panorama_capacity(rig_);
+            o.panorama = f.pano.get<std::uint8_t>(o.pano_cap);
+            o.homographies = f.homs.get<lp_homography>(ncams);
+            int* counts = f.counts.get<int>(ncams + np);
+            o.kp_counts = counts;
+            o.match_counts = counts + ncams;
+            o.keypoints = f.kps.get<lp_keypoint>(static_cast<std::size_t>(ncams) * cap_kp);
+            o.descriptors = f.desc.get<std::uint64_t>(static_cast<std::size_t>(ncams) * cap_kp * W2);
             o.cap_kp = cap_kp;
-            o.match_counts = f->match_counts.data();
-            o.matches = f->matches.data();
+            o.matches = f.matches.get<lp_match>(np * cap_kp);
             o.cap_matches = cap_kp;
+            std::uint8_t* staged = f.frames.get<std::uint8_t>(ncams * fb);
             std::vector<const std::uint8_t*> ims(ncams);
-            for (int c = 0; c < ncams; ++c) ims[c] = p.images[c].data.data();
-            f->t_submit = detail::now_ns();
-            const lp_status st = lp_rig_submit_frame(rig_, ims.data(), p.frame_index, &o, &f->ticket);
+            for (int c = 0; c < ncams; ++c) {
+                std::memcpy(staged + c * fb, p.images[c].data.data(), fb);
+                ims[c] = staged + c * fb;
+            }
+            f.t_submit = detail::now_ns();
+            const lp_status st = lp_rig_submit_frame(rig_, ims.data(), p.frame_index, &o, &f.ticket);
             if (st != LP_OK) {
                 note_drop(p, stage_of(st), lp_last_error(), m);
-                f->ticket = 0;
+                f.ticket = 0;
             }
         } catch (const std::exception& e) {
             note_drop(p, Stage::Detect, e.what(), m);
-            f->ticket = 0;
+            f.ticket = 0;
         }
-        f->pkt = std::move(pkt);
-        return f;
     }
 
     // the frame back from the device into its packet, then to the sink
@@ -785,8 +803,8 @@ private:
         const int W2 = 2 * Descriptor::words(n_d);
         for (int c = 0; c < ncams; ++c) {
             const int n = std::min(o.kp_counts[c], o.cap_kp);
-            const lp_keypoint* k = f.kps.data() + static_cast<std::size_t>(c) * o.cap_kp;
-            const std::uint64_t* d = f.desc.data() + static_cast<std::size_t>(c) * o.cap_kp * W2;
+            const lp_keypoint* k = o.keypoints + static_cast<std::size_t>(c) * o.cap_kp;
+            const std::uint64_t* d = o.descriptors + static_cast<std::size_t>(c) * o.cap_kp * W2;
             for (int i = 0; i < n; ++i) {
                 p.keypoints[c].push_back(Keypoint{k[i].x, k[i].y, k[i].response, k[i].region_id});
                 p.descriptors[c].push_back(b200::unpack(d + static_cast<std::size_t>(i) * W2, n_d));
@@ -795,7 +813,7 @@ private:
         if (o.estimated) {
             for (int q = 0; q + 1 < ncams; ++q) {
                 const int n = std::min(o.match_counts[q], o.cap_matches);
-                const lp_match* mm = f.matches.data() + static_cast<std::size_t>(q) * o.cap_matches;
+                const lp_match* mm = o.matches + static_cast<std::size_t>(q) * o.cap_matches;
                 for (int i = 0; i < n; ++i)
                     p.pair_matches[q].push_back(Match{mm[i].query_id, mm[i].train_id, mm[i].distance, mm[i].quality});
             }
@@ -803,7 +821,7 @@ private:
         p.homographies.clear();
         for (int c = 0; c < ncams; ++c) {
             Homography h;
-            std::memcpy(h.h.data(), f.homs[c].h, sizeof f.homs[c].h);
+            std::memcpy(h.h.data(), o.homographies[c].h, sizeof o.homographies[c].h);
             p.homographies.push_back(h);
         }
         if (o.estimated) cache_.record_device_estimate(p.homographies);
@@ -811,8 +829,7 @@ private:
         p.composite.height = o.canvas.height;
         p.composite.channels = 1;
         p.composite.color_space = ColorSpace::Gray;
-        p.composite.data.assign(f.pano.begin(),
-                                f.pano.begin() + static_cast<std::size_t>(o.canvas.width) * o.canvas.height);
+        p.composite.data.assign(o.panorama, o.panorama + static_cast<std::size_t>(o.canvas.width) * o.canvas.height);
         // device stage times (detect + describe are one fused sequence)
         const double ms_to_ns = 1e6;
         const double dev[4] = {o.stage_ms[0], 0.0, o.stage_ms[2], o.stage_ms[3]};
@@ -837,6 +854,7 @@ private:
     bool warmup_noted_ = false;
     lp_rig* rig_ = nullptr;
     int rig_cams_ = 0, rig_w_ = 0, rig_h_ = 0;
+    std::array<Flight, 3> flights_;
 };
 
 /// A pool sized for `frames_in_flight` packets (pipeline.hpp:724-735).

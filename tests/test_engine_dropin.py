@@ -49,6 +49,7 @@ def test_stitch_engine_dropin_cfg1():
     short = _run("engine_bench_b200", "cfg1", 20, "serial")
     _record("cfg1", {"reference_cpu": ref, "b200_serial": ser, "b200_pipelined": pip})
     assert short["composite_fnv"] == ref["composite_fnv"] and short["composite_sum"] == ref["composite_sum"]
+    assert short["first_fnv"] == ref["first_fnv"]
     assert ser["composite_fnv"] == pip["composite_fnv"]
     assert ser["estimations"] == pip["estimations"] == 300
     assert ser["drops"] == pip["drops"] == 0
