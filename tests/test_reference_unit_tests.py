@@ -46,8 +46,10 @@ def test_reference_unit_tests_on_b200_dropin(tmp_path):
 
 
 # The reference's acceptance suite (proj/tests/acceptance.cpp, 12 criteria,
-# unmodified). Criteria 8 and 9 are CPU-cost ratios (strip vs full-frame
-# extraction time, the thread pipeline's speedup over serial). On the GPU a
+# unmodified). Criterion 9 (Pipelined >= 1.5x Serial, byte-identical) runs
+# through the drop-in pipeline.hpp, whose Pipelined mode keeps 3 frames on the
+# device (2.1x on the B200 box, profiles/r2_acceptance_b200.log). Criterion 8
+# is a CPU-cost ratio (strip vs full-frame extraction time). On the GPU a
 # host-image call moves only the used rectangle, so the strip costs 0.12 ms
 # against 0.19 ms for the full frame (ratio ~0.6, scripts/probes/
 # extract_timing.py): both describe the same top_n=500 keypoints and pay the
@@ -55,7 +57,7 @@ def test_reference_unit_tests_on_b200_dropin(tmp_path):
 # microseconds, so criterion 9's thread speedup does not describe the device. Criterion 11 needs the CLI:
 # the B200 build drives this repo's CLI, the reference build has none (CLI11
 # absent here), and criterion 9 depends on the host's thread count.
-ACCEPT_B200_EXPECTED = {8, 9}
+ACCEPT_B200_EXPECTED = {8}
 ACCEPT_REF_EXPECTED = {9, 11}
 
 
@@ -80,4 +82,4 @@ def test_acceptance_on_reference(tmp_path):
 def test_acceptance_on_b200_dropin(tmp_path):
     passed, failed, log = _accept(_ensure("acceptance_b200"), tmp_path)
     assert failed <= ACCEPT_B200_EXPECTED, log
-    assert {1, 2, 3, 4, 5, 6, 7, 10, 11, 12} <= passed, log
+    assert {1, 2, 3, 4, 5, 6, 7, 9, 10, 11, 12} <= passed, log
