@@ -50,13 +50,12 @@ def test_reference_unit_tests_on_b200_dropin(tmp_path):
 # through the drop-in pipeline.hpp, whose Pipelined mode keeps 3 frames on the
 # device (2.1x on the B200 box, profiles/r2_acceptance_b200.log). Criterion 8
 # is a CPU-cost ratio (strip vs full-frame extraction time). On the GPU a
-# host-image call moves only the used rectangle, so the strip costs 0.12 ms
-# against 0.19 ms for the full frame (ratio ~0.6, scripts/probes/
-# extract_timing.py): both describe the same top_n=500 keypoints and pay the
-# same launch + one-sync floor, so the 0.4 bound cannot hold; the stages are
-# microseconds, so criterion 9's thread speedup does not describe the device. Criterion 11 needs the CLI:
-# the B200 build drives this repo's CLI, the reference build has none (CLI11
-# absent here), and criterion 9 depends on the host's thread count.
+# host-image call moves only the used rectangle, so the strip costs 0.1 ms
+# against 0.2 ms for the full frame (ratio ~0.63, the log above): both
+# describe the same top_n=500 keypoints and pay the same launch + one-sync
+# floor, so the 0.4 bound does not hold. Criterion 11 needs the CLI: the B200
+# build drives this repo's CLI, the reference build has none (CLI11 absent
+# here); the reference's criterion 9 depends on the host's thread count.
 ACCEPT_B200_EXPECTED = {8}
 ACCEPT_REF_EXPECTED = {9, 11}
 
