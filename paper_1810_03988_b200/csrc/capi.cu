@@ -8,7 +8,7 @@
 // one PROSAC launch, and the compositor runs once per frame; device arenas are
 // sized at creation like BufferPool (pipeline.hpp:68-109) and the homography
 // cache follows HomographyCache (pipeline.hpp:259-286).
-#include <cub/cub.cuh>
+#include "prims.cuh"
 
 #include <atomic>
 #include <cctype>
@@ -353,6 +353,44 @@ struct lp_ctx {
     }
 };
 
+namespace lpb {
+// compaction writers (prims.cuh: k_flag_scatter)
+struct WriteXY {  // scan-area index -> (x, y)
+    int* xy;
+    int x0, sw, y0, cap;
+    __device__ void operator()(int i, int j) const {
+        if (j < cap) {
+            xy[2 * j] = x0 + i % sw;
+            xy[2 * j + 1] = y0 + i / sw;
+        }
+    }
+};
+struct WriteKp {  // kept keypoints in input order
+    const lp_keypoint* in;
+    lp_keypoint* out;
+    __device__ void operator()(int i, int j) const { out[j] = in[i]; }
+};
+
+// count the flags, then scatter the survivors (input order) with `write`
+// into the output the caller sizes from the count: returns the count
+template <class MakeWriter>
+static int compact_flags(const uint8_t* flags, int n, cudaStream_t s, MakeWriter make_writer) {
+    const int tiles = cdiv(n, kPrimTile);
+    DBuf off(sizeof(unsigned) * tiles, s), tot(sizeof(int), s);
+    LPB_LAUNCH(k_flag_count, tiles, 256, 0, s, flags, n, off.as<unsigned>());
+    LPB_LAUNCH(k_scan_exclusive, 1, 1024, 0, s, off.as<unsigned>(), tiles, tot.as<int>());
+    int total = 0;
+    LPB_CUDA(cudaMemcpyAsync(&total, tot.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LPB_CUDA(cudaStreamSynchronize(s));
+    if (total > 0) {
+        auto w = make_writer(total);
+        LPB_LAUNCH(k_flag_scatter<decltype(w)>, tiles, 256, 0, s, flags, n, off.as<unsigned>(), w);
+    }
+    return total;
+}
+
+}  // namespace lpb
+
 extern "C" {
 
 const char* lp_last_error(void) { return g_err.c_str(); }
@@ -458,12 +496,6 @@ __global__ void k_iota(int* p, int n) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = i;
 }
-__global__ void k_xy_from_index(const int* idx, int n, int x0, int sw, int y0, int* xy) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    xy[2 * i] = x0 + idx[i] % sw;
-    xy[2 * i + 1] = y0 + idx[i] / sw;
-}
 
 lp_status lp_fast_corners(lp_ctx* ctx, const uint8_t* img, int w, int h, int ch, lp_region r,
                           int thr, int arc, int* xy_out, int cap, int* count) {
@@ -476,23 +508,16 @@ lp_status lp_fast_corners(lp_ctx* ctx, const uint8_t* img, int w, int h, int ch,
         In<uint8_t> dimg(img, static_cast<size_t>(w) * h, s);
         const int sw = x1 - x0;
         const int n = sw * (y1 - y0);
-        DBuf flags(n, s), idx(sizeof(int) * n, s), nsel(sizeof(int), s), lin(sizeof(int) * n, s);
+        DBuf flags(n, s);
         fast_flags_launch(dimg.d, w, h, x0, y0, x1, y1, static_cast<uint8_t>(thr), arc, flags.as<uint8_t>(), s);
-        LPB_LAUNCH(k_iota, cdiv(n, 256), 256, 0, s, lin.as<int>(), n);
-        size_t tb = 0;
-        const int* it = lin.as<int>();
-        cub::DeviceSelect::Flagged(nullptr, tb, it, flags.as<uint8_t>(), idx.as<int>(), nsel.as<int>(), n, s);
-        DBuf tmp(tb, s);
-        cub::DeviceSelect::Flagged(tmp.p, tb, it, flags.as<uint8_t>(), idx.as<int>(), nsel.as<int>(), n, s);
-        int total = 0;
-        LPB_CUDA(cudaMemcpyAsync(&total, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-        LPB_CUDA(cudaStreamSynchronize(s));
-        const int k = std::min(total, cap);
-        Out<int> dxy(xy_out, static_cast<size_t>(2) * k, s);
-        if (k > 0) {
-            LPB_LAUNCH(k_xy_from_index, cdiv(k, 256), 256, 0, s, idx.as<int>(), k, x0, sw, y0, dxy.d);
-            dxy.finish(s, static_cast<size_t>(2) * k);
-        }
+        std::unique_ptr<Out<int>> dxy;
+        int k = 0;
+        const int total = lpb::compact_flags(flags.as<uint8_t>(), n, s, [&](int t) {
+            k = std::min(t, cap);
+            dxy = std::make_unique<Out<int>>(xy_out, static_cast<size_t>(2) * std::max(k, 1), s);
+            return lpb::WriteXY{dxy->d, x0, sw, y0, k};
+        });
+        if (k > 0) dxy->finish(s, static_cast<size_t>(2) * k);
         LPB_CUDA(cudaStreamSynchronize(s));
         *count = total;
     });
@@ -518,43 +543,62 @@ lp_status lp_harris_response(lp_ctx* ctx, const uint8_t* img, int w, int h, int 
     });
 }
 
+// bounding box of the candidates (lorb.hpp:258-266) on the device
+__global__ void k_kp_bbox(const lp_keypoint* kp, int n, int* box) {
+    int mnx = INT_MAX, mny = INT_MAX, mxx = INT_MIN, mxy = INT_MIN;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        mnx = min(mnx, kp[i].x);
+        mxx = max(mxx, kp[i].x);
+        mny = min(mny, kp[i].y);
+        mxy = max(mxy, kp[i].y);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mnx = min(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+        mxx = max(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+        mny = min(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+        mxy = max(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(box, mnx);
+        atomicMax(box + 1, mxx);
+        atomicMin(box + 2, mny);
+        atomicMax(box + 3, mxy);
+    }
+}
+
 lp_status lp_nms(lp_ctx* ctx, const lp_keypoint* in, int n, int radius, lp_keypoint* out, int* count) {
     return guard([&] {
         *count = 0;
         if (n == 0) return;
         cudaStream_t s = ctx->stream;
-        std::vector<lp_keypoint> hk(n);
+        // the grid needs the candidates' bounding box on the host (its size):
+        // host input is scanned here, device input reduced on the device
+        In<lp_keypoint> dk(in, n, s);
+        int box[4] = {INT_MAX, INT_MIN, INT_MAX, INT_MIN};
         if (is_device_ptr(in)) {
-            LPB_CUDA(cudaMemcpyAsync(hk.data(), in, sizeof(lp_keypoint) * n, cudaMemcpyDeviceToHost, s));
+            DBuf db(sizeof box, s);
+            LPB_CUDA(cudaMemcpyAsync(db.p, box, sizeof box, cudaMemcpyHostToDevice, s));
+            LPB_LAUNCH(k_kp_bbox, std::min(cdiv(n, 256), 1184), 256, 0, s, dk.d, n, db.as<int>());
+            LPB_CUDA(cudaMemcpyAsync(box, db.p, sizeof box, cudaMemcpyDeviceToHost, s));
             LPB_CUDA(cudaStreamSynchronize(s));
         } else {
-            std::memcpy(hk.data(), in, sizeof(lp_keypoint) * n);
+            for (int i = 0; i < n; ++i) {
+                box[0] = std::min(box[0], in[i].x);
+                box[1] = std::max(box[1], in[i].x);
+                box[2] = std::min(box[2], in[i].y);
+                box[3] = std::max(box[3], in[i].y);
+            }
         }
-        int minx = hk[0].x, maxx = hk[0].x, miny = hk[0].y, maxy = hk[0].y;
-        for (auto& k : hk) {
-            minx = std::min(minx, k.x);
-            maxx = std::max(maxx, k.x);
-            miny = std::min(miny, k.y);
-            maxy = std::max(maxy, k.y);
-        }
-        const int gw = maxx - minx + 1, gh = maxy - miny + 1;
-        DBuf dk = upload(hk, s);
-        DBuf grid(sizeof(int) * static_cast<size_t>(gw) * gh, s), keep(n, s), sel(sizeof(lp_keypoint) * n, s),
-            nsel(sizeof(int), s);
-        nms_generic_launch(dk.as<lp_keypoint>(), n, radius, minx, miny, gw, gh, grid.as<int>(), keep.as<uint8_t>(), s);
-        size_t tb = 0;
-        cub::DeviceSelect::Flagged(nullptr, tb, dk.as<lp_keypoint>(), keep.as<uint8_t>(), sel.as<lp_keypoint>(),
-                                   nsel.as<int>(), n, s);
-        DBuf tmp(tb, s);
-        cub::DeviceSelect::Flagged(tmp.p, tb, dk.as<lp_keypoint>(), keep.as<uint8_t>(), sel.as<lp_keypoint>(),
-                                   nsel.as<int>(), n, s);
-        int k = 0;
-        LPB_CUDA(cudaMemcpyAsync(&k, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-        LPB_CUDA(cudaStreamSynchronize(s));
-        if (is_device_ptr(out))
-            LPB_CUDA(cudaMemcpyAsync(out, sel.p, sizeof(lp_keypoint) * k, cudaMemcpyDeviceToDevice, s));
-        else
-            LPB_CUDA(cudaMemcpyAsync(out, sel.p, sizeof(lp_keypoint) * k, cudaMemcpyDeviceToHost, s));
+        const int minx = box[0], miny = box[2];
+        const int gw = box[1] - minx + 1, gh = box[3] - miny + 1;
+        DBuf grid(sizeof(int) * static_cast<size_t>(gw) * gh, s), keep(n, s);
+        nms_generic_launch(dk.d, n, radius, minx, miny, gw, gh, grid.as<int>(), keep.as<uint8_t>(), s);
+        std::unique_ptr<Out<lp_keypoint>> dout;
+        const int k = lpb::compact_flags(keep.as<uint8_t>(), n, s, [&](int t) {
+            dout = std::make_unique<Out<lp_keypoint>>(out, static_cast<size_t>(t), s);
+            return lpb::WriteKp{dk.d, dout->d};
+        });
+        if (k > 0) dout->finish(s, static_cast<size_t>(k));
         LPB_CUDA(cudaStreamSynchronize(s));
         *count = k;
     });
@@ -565,7 +609,7 @@ __global__ void k_sort_key(const lp_keypoint* kp, const int* idx, int n, int fie
     if (i >= n) return;
     const lp_keypoint k = kp[idx[i]];
     key[i] = field == 0 ? (static_cast<uint32_t>(k.x) ^ 0x80000000u)
-                        : field == 1 ? (static_cast<uint32_t>(k.y) ^ 0x80000000u) : float_key(k.response);
+                        : field == 1 ? (static_cast<uint32_t>(k.y) ^ 0x80000000u) : ~float_key(k.response);
 }
 __global__ void k_gather_kp(const lp_keypoint* kp, const int* idx, int n, lp_keypoint* out) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -580,22 +624,15 @@ lp_status lp_select_top_n(lp_ctx* ctx, const lp_keypoint* in, int n, int top_n, 
         if (n == 0) return;
         cudaStream_t s = ctx->stream;
         In<lp_keypoint> dk(in, n, s);
-        DBuf ia(sizeof(int) * n, s), ib(sizeof(int) * n, s), ka(sizeof(uint32_t) * n, s), kb(sizeof(uint32_t) * n, s);
+        DBuf ia(sizeof(int) * n, s), ib(sizeof(int) * n, s), ka(sizeof(uint32_t) * n, s), kb(sizeof(uint32_t) * n, s),
+            hist(sizeof(unsigned) * 256 * cdiv(n, kPrimTile), s);
         LPB_LAUNCH(k_iota, cdiv(n, 256), 256, 0, s, ia.as<int>(), n);
-        size_t tb = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tb, ka.as<uint32_t>(), kb.as<uint32_t>(), ia.as<int>(), ib.as<int>(), n,
-                                        0, 32, s);
-        DBuf tmp(tb, s);
-        // stable LSD passes: x asc, then y asc, then response desc (lorb.hpp:293-296)
+        // stable LSD passes: x asc, then y asc, then response desc (its key
+        // inverted) (lorb.hpp:293-296); prims.cuh radix sort, result in (ka, ia)
         for (int field = 0; field < 3; ++field) {
             LPB_LAUNCH(k_sort_key, cdiv(n, 256), 256, 0, s, dk.d, ia.as<int>(), n, field, ka.as<uint32_t>());
-            if (field < 2)
-                cub::DeviceRadixSort::SortPairs(tmp.p, tb, ka.as<uint32_t>(), kb.as<uint32_t>(), ia.as<int>(),
-                                                ib.as<int>(), n, 0, 32, s);
-            else
-                cub::DeviceRadixSort::SortPairsDescending(tmp.p, tb, ka.as<uint32_t>(), kb.as<uint32_t>(),
-                                                          ia.as<int>(), ib.as<int>(), n, 0, 32, s);
-            LPB_CUDA(cudaMemcpyAsync(ia.p, ib.p, sizeof(int) * n, cudaMemcpyDeviceToDevice, s));
+            radix_sort_pairs(ka.as<uint32_t>(), ia.as<int>(), kb.as<uint32_t>(), ib.as<int>(), n, 32,
+                             hist.as<unsigned>(), s);
         }
         const int k = std::min(n, top_n);
         Out<lp_keypoint> dout(out, k, s);

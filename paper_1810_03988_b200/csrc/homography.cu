@@ -17,7 +17,6 @@
 //    warp Jacobi SVD of the 9x9 factor.
 // Compiled with --fmad=false: every FP64 expression rounds like the x86 oracle.
 #include <cooperative_groups.h>
-#include <cub/block/block_scan.cuh>
 
 #include "homography.cuh"
 #include <math_constants.h>
@@ -654,19 +653,22 @@ __device__ int dlt_block(const lp_corr* p, const int* idx, int m, double* A, dou
 // returns the count on every thread
 template <typename F>
 __device__ int block_compact(int n, int* idx, F flag) {
-    using Scan = cub::BlockScan<int, 256>;
-    __shared__ typename Scan::TempStorage tmp;
-    __shared__ int s_total;
+    __shared__ int s_w[8];  // survivors per warp of the current 256
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int base = 0;
     for (int b0 = 0; b0 < n; b0 += 256) {
         const int i = b0 + threadIdx.x;
-        const int f = (i < n && flag(i)) ? 1 : 0;
-        int pos, total;
-        Scan(tmp).ExclusiveSum(f, pos, total);
-        if (f) idx[base + pos] = i;
-        if (threadIdx.x == 0) s_total = total;
+        const bool f = i < n && flag(i);
+        const unsigned m = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) s_w[warp] = __popc(m);
         __syncthreads();
-        base += s_total;
+        int pos = base, total = 0;
+        for (int w = 0; w < 8; ++w) {
+            pos += w < warp ? s_w[w] : 0;
+            total += s_w[w];
+        }
+        if (f) idx[pos + __popc(m & ((1u << lane) - 1u))] = i;
+        base += total;
         __syncthreads();
     }
     return base;

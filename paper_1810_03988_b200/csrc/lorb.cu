@@ -19,7 +19,6 @@
 //              (lorb.hpp:333-350). Values equal the reference's region-crop
 //              blur at every sampled point (test_lorb.cpp:301-343).
 // All FP ops are explicit round-to-nearest (no FMA), matching the reference.
-#include <cub/cub.cuh>
 
 #include "lorb.cuh"
 

@@ -65,6 +65,33 @@ def test_nms_topn(lp, orc):
         assert np.array_equal(lp.select_top_n(kq, n), orc.select_top_n(kq, n))
 
 
+def test_select_top_n_and_nms_large(lp, orc):
+    """The repo's own compaction and radix sort (csrc/prims.cuh) behind
+    lp_nms / lp_select_top_n over many tiles: 300K candidates with heavily
+    tied responses and negative coordinates, host and device inputs."""
+    import torch
+    rng = np.random.default_rng(5)
+    n = 300_000
+    kp = np.zeros((n, 4), np.int32)
+    kp[:, 0] = rng.integers(-50, 1500, n)
+    kp[:, 1] = rng.integers(-20, 900, n)
+    kp[:, 2] = rng.integers(0, 64, n).astype(np.float32).view(np.int32)
+    kp[:, 3] = rng.integers(0, 6, n)
+    # unique positions (the reference's grid keeps one candidate per cell)
+    _, first = np.unique(kp[:, 0].astype(np.int64) * 4096 + kp[:, 1], return_index=True)
+    kp = kp[np.sort(first)]
+    for top_n in (1, 777, 50_000, len(kp)):
+        assert np.array_equal(lp.select_top_n(kp, top_n), orc.select_top_n(kp, top_n)), top_n
+    want = orc.nms(kp, 1)
+    assert np.array_equal(lp.nms(kp, 1), want)
+    import ctypes as C
+    dev = torch.from_numpy(kp).cuda()
+    out = np.zeros_like(kp)
+    cnt = C.c_int()
+    lp._call("nms", C.c_void_p(dev.data_ptr()), len(kp), 1, out.ctypes.data_as(C.c_void_p), C.byref(cnt))
+    assert np.array_equal(out[:cnt.value], want)
+
+
 @pytest.mark.parametrize("sigma,ch", [(1.0, 1), (2.0, 1), (1.5, 3)])
 def test_gaussian_blur(lp, orc, sigma, ch):
     rng = np.random.default_rng(1)
