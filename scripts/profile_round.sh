@@ -14,7 +14,7 @@ export LPB_GRAPHS=0   # individual launches (graph nodes are otherwise one launc
 # frame 0 registers (18 kernels); config 3 then runs 13 per frame, config 1 (re-registering
 # every frame) 18: capture the third frame whole, starting at its k_detect9
 for CFG in cfg3 cfg1; do
-  if [ $CFG = cfg3 ]; then SKIP=31; CNT=13; else SKIP=36; CNT=18; fi
+  if [ $CFG = cfg3 ]; then SKIP=${SKIP3:-33}; CNT=${CNT3:-14}; else SKIP=${SKIP1:-38}; CNT=${CNT1:-19}; fi
   timeout 900 ncu --set full --clock-control none -k regex:"^(lpb::)?k_" -s $SKIP -c $CNT \
       -o gpurun_out/frame_$CFG -f python bench.py --config $CFG --steps 3 --warmup 1 --no-e2e \
       --no-cpu-baseline --no-profile > gpurun_out/frame_${CFG}_$TAG.log 2>&1
