@@ -155,34 +155,6 @@ static bool is_device_ptr(const void* p) {
 }
 
 // stream-ordered scratch buffer
-struct DBuf {
-    void* p = nullptr;
-    cudaStream_t s = nullptr;
-    DBuf() = default;
-    DBuf(size_t bytes, cudaStream_t st) : s(st) {
-        if (bytes) LPB_CUDA(cudaMallocAsync(&p, bytes, st));
-    }
-    DBuf(const DBuf&) = delete;
-    DBuf& operator=(const DBuf&) = delete;
-    DBuf(DBuf&& o) noexcept : p(o.p), s(o.s) { o.p = nullptr; }
-    DBuf& operator=(DBuf&& o) noexcept {
-        if (this != &o) {
-            if (p) cudaFreeAsync(p, s);
-            p = o.p;
-            s = o.s;
-            o.p = nullptr;
-        }
-        return *this;
-    }
-    ~DBuf() {
-        if (p) cudaFreeAsync(p, s);
-    }
-    template <class T>
-    T* as() const {
-        return static_cast<T*>(p);
-    }
-};
-
 // device view of a caller buffer (copy-in for host memory)
 template <class T>
 struct In {

@@ -94,6 +94,35 @@ inline void ensure_dyn_smem(const void* kernel, int bytes) {
     throw Status(LP_INTERNAL, "ensure_dyn_smem: slot table full");
 }
 
+// stream-ordered device allocation (cudaMallocAsync / cudaFreeAsync)
+struct DBuf {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    DBuf() = default;
+    DBuf(size_t bytes, cudaStream_t st) : s(st) {
+        if (bytes) LPB_CUDA(cudaMallocAsync(&p, bytes, st));
+    }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), s(o.s) { o.p = nullptr; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            if (p) cudaFreeAsync(p, s);
+            p = o.p;
+            s = o.s;
+            o.p = nullptr;
+        }
+        return *this;
+    }
+    ~DBuf() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
 // device-side status word: first error wins (atomicCAS from 0)
 __device__ __forceinline__ void dev_fail(int* status, int code) {
     atomicCAS(status, 0, code);

@@ -12,6 +12,7 @@
 // (quality desc, query_id asc) = (distance asc, query_id asc) by rank
 // placement and emits the Correspondence list for PROSAC (pipeline.hpp:480-488).
 #include "match.cuh"
+#include "prims.cuh"
 
 namespace lpb {
 
@@ -72,6 +73,7 @@ __device__ __forceinline__ void top2_insert(int d, int j, int& d0, int& j0, int&
 }
 
 constexpr int kMaxW = 8;  // n_d <= 512
+constexpr int kFinalizeSmemMax = 64 << 10;  // k_match_finalize's key array (16K accepted matches)
 
 // one warp per query (large problems: enough warps, and a small register
 // footprint keeps 6 CTAs per SM resident)
@@ -261,6 +263,54 @@ __global__ void __launch_bounds__(1024) k_match_finalize(MatchArgs a) {
     if (threadIdx.x == 0) a.match_counts[pair] = n;
 }
 
+// Large pairs (more accepted matches than k_match_finalize's shared-memory
+// rank placement holds): every query writes its (distance, query) key, or
+// ~0 if rejected, at its own index; a stable radix sort of the cap keys
+// (prims.cuh) orders them, and the emitter writes rank i from sorted key i.
+__global__ void k_match_keys(MatchArgs a, int pair, uint32_t* keys) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= a.cap) return;
+    const int qs = a.qslot0 + pair, nq = a.counts[qs], nt = a.counts[a.tslot0 + pair];
+    uint32_t k = ~0u;
+    if (q < nq && nt > 0) {
+        const int4 r = a.qres[static_cast<size_t>(pair) * a.cap + q];
+        if (r.x >= 0 && !(r.z >= 0 && !(static_cast<float>(r.y) < fmul(a.ratio, static_cast<float>(r.z)))))
+            k = (static_cast<uint32_t>(r.y) << 21) | static_cast<uint32_t>(q);
+    }
+    keys[q] = k;
+}
+__global__ void k_match_emit(MatchArgs a, int pair, const uint32_t* keys) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.cap) return;
+    const int qs = a.qslot0 + pair, ts = a.tslot0 + pair;
+    if (i == 0 && (a.counts[qs] == 0 || a.counts[ts] == 0)) {
+        dev_fail(a.pair_status + pair, LP_EMPTY_INPUT);
+        a.match_counts[pair] = 0;
+    }
+    const uint32_t key = keys[i];
+    if (key == ~0u) return;
+    if (i + 1 == a.cap || keys[i + 1] == ~0u) a.match_counts[pair] = i + 1;
+    const int q = static_cast<int>(key & 0x1FFFFFu), d = static_cast<int>(key >> 21);
+    const int4 qr = a.qres[static_cast<size_t>(pair) * a.cap + q];
+    lp_match m;
+    m.query_id = q;
+    m.train_id = qr.x;
+    m.distance = d;
+    m.quality = fsub(1.0f, __fdiv_rn(static_cast<float>(d), fmul(2.0f, static_cast<float>(a.n_d))));
+    a.matches[static_cast<size_t>(pair) * a.cap + i] = m;
+    const lp_keypoint sk = a.kps[static_cast<size_t>(qs) * a.cap + q];
+    const lp_keypoint tk = a.kps[static_cast<size_t>(ts) * a.cap + qr.x];
+    lp_corr c;
+    c.sx = static_cast<double>(sk.x);
+    c.sy = static_cast<double>(sk.y);
+    c.dx = static_cast<double>(tk.x);
+    c.dy = static_cast<double>(tk.y);
+    c.quality = m.quality;
+    c.pad_ = 0;
+    a.corr[static_cast<size_t>(pair) * a.cap + i] = c;
+}
+__global__ void k_zero_int(int* p) { *p = 0; }
+
 void match_launch(const MatchArgs& a, cudaStream_t s) {
     if (a.npairs <= 0) return;
     if (a.n_d > 64 * kMaxW) throw Status(LP_BAD_PARAMS, "match: n_d too large");
@@ -280,8 +330,21 @@ void match_launch(const MatchArgs& a, cudaStream_t s) {
     int p2 = 1;
     while (p2 < a.cap) p2 <<= 1;
     const int smem = p2 * 4;
-    ensure_dyn_smem(reinterpret_cast<const void*>(k_match_finalize), smem);
-    LPB_LAUNCH(k_match_finalize, a.npairs, 1024, smem, s, a);
+    if (smem <= kFinalizeSmemMax) {  // O(n^2 / 1024) rank placement in shared memory
+        ensure_dyn_smem(reinterpret_cast<const void*>(k_match_finalize), smem);
+        LPB_LAUNCH(k_match_finalize, a.npairs, 1024, smem, s, a);
+        return;
+    }
+    const int tiles = cdiv(a.cap, kPrimTile);
+    DBuf ka(sizeof(uint32_t) * a.cap, s), kb(sizeof(uint32_t) * a.cap, s), va(sizeof(int) * a.cap, s),
+        vb(sizeof(int) * a.cap, s), hist(sizeof(unsigned) * 256 * tiles, s);
+    for (int p = 0; p < a.npairs; ++p) {
+        LPB_LAUNCH(k_match_keys, cdiv(a.cap, 256), 256, 0, s, a, p, ka.as<uint32_t>());
+        radix_sort_pairs(ka.as<uint32_t>(), va.as<int>(), kb.as<uint32_t>(), vb.as<int>(), a.cap, 32,
+                         hist.as<unsigned>(), s);
+        LPB_LAUNCH(k_zero_int, 1, 1, 0, s, a.match_counts + p);
+        LPB_LAUNCH(k_match_emit, cdiv(a.cap, 256), 256, 0, s, a, p, ka.as<uint32_t>());
+    }
 }
 
 }  // namespace lpb

@@ -14,7 +14,7 @@ constexpr int kPrimTile = 2048;  // elements per tile: 8 rounds x 256 threads
 
 // ---- exclusive scan of n ints in place by one CTA (carry across chunks);
 // *total (optional) gets the sum
-__global__ void __launch_bounds__(1024) k_scan_exclusive(unsigned* a, int n, int* total) {
+static __global__ void __launch_bounds__(1024) k_scan_exclusive(unsigned* a, int n, int* total) {
     __shared__ unsigned s_warp[32];
     __shared__ unsigned s_carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(1024) k_scan_exclusive(unsigned* a, int n, int
 }
 
 // ---- compaction: counts per tile, then scatter by ballot ranks
-__global__ void __launch_bounds__(256) k_flag_count(const uint8_t* flags, int n, unsigned* tile_count) {
+static __global__ void __launch_bounds__(256) k_flag_count(const uint8_t* flags, int n, unsigned* tile_count) {
     const int base = blockIdx.x * kPrimTile;
     int c = 0;
 #pragma unroll
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) k_flag_count(const uint8_t* flags, int n,
 
 // write(i, j): flagged element i is the j-th survivor
 template <class W>
-__global__ void __launch_bounds__(256) k_flag_scatter(const uint8_t* flags, int n, const unsigned* tile_off, W write) {
+static __global__ void __launch_bounds__(256) k_flag_scatter(const uint8_t* flags, int n, const unsigned* tile_off, W write) {
     __shared__ unsigned s_w[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int base = blockIdx.x * kPrimTile;
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) k_flag_scatter(const uint8_t* flags, int 
 
 // ---- stable LSD radix sort pass (8-bit digit at `shift`) of 32-bit keys
 // with int payloads
-__global__ void __launch_bounds__(256) k_radix_hist(const uint32_t* keys, int n, int shift, unsigned* hist,
+static __global__ void __launch_bounds__(256) k_radix_hist(const uint32_t* keys, int n, int shift, unsigned* hist,
                                                      int ntiles) {
     __shared__ unsigned s_h[256];
     s_h[threadIdx.x] = 0;
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(256) k_radix_hist(const uint32_t* keys, int n,
     hist[threadIdx.x * ntiles + blockIdx.x] = s_h[threadIdx.x];  // digit-major: one scan orders digits, then tiles
 }
 
-__global__ void __launch_bounds__(256) k_radix_scatter(const uint32_t* kin, const int* vin, int n, int shift,
+static __global__ void __launch_bounds__(256) k_radix_scatter(const uint32_t* kin, const int* vin, int n, int shift,
                                                         const unsigned* off, int ntiles, uint32_t* kout, int* vout) {
     __shared__ unsigned s_wc[8][256];  // this round: elements per (warp, digit)
     __shared__ unsigned s_run[256];    // this tile so far: elements per digit

@@ -181,6 +181,28 @@ def test_match_features(lp, orc, params):
     mc2.t_probes, mc2.tables, mc2.bits = 16, 4, 16
 
 
+def test_match_features_large_sets(lp, orc, params):
+    """More accepted matches than k_match_finalize's shared-memory rank
+    placement holds (> 16K): the radix-sorted finalize path (match.cu,
+    prims.cuh). 20K train descriptors, 20K queries that are noisy copies."""
+    rng = np.random.default_rng(11)
+    n = 20_000
+    train = rng.integers(0, 2**63, size=(n, 8), dtype=np.uint64)
+    train[:, 4:] &= ~train[:, :4]  # ternary planes disjoint
+    query = train.copy()
+    flips = rng.integers(0, 256, size=(n, 3))
+    for i, f in enumerate(flips):
+        for b_ in f:
+            query[i, b_ // 64] ^= np.uint64(1) << np.uint64(b_ % 64)
+    query[:, 4:] &= ~query[:, :4]
+    perm = rng.permutation(n)
+    query = query[perm]
+    mc = params.matching
+    a = lp.match_features(query, train, 256, mc)
+    b = orc.match_features(query, train, 256, mc)
+    assert len(a) > 16_384 and np.array_equal(a, b)
+
+
 def test_descriptor_distances(lp, orc):
     rng = np.random.default_rng(0)
     a = rng.integers(0, 2**63, size=(50, 8), dtype=np.uint64)
