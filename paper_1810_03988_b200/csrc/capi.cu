@@ -234,7 +234,6 @@ static void validate_ext(const lp_extraction_config& c) {  // lorb.hpp:82-89
     if (!(c.harris_sigma > 0.0f)) throw Status(LP_INVALID_SIGMA, "harris_sigma must be > 0");
     if (!(c.brief_blur_sigma > 0.0f)) throw Status(LP_INVALID_SIGMA, "brief_blur_sigma must be > 0");
     if (c.patch_half < 1) throw Status(LP_BAD_PARAMS, "patch_half must be >= 1");
-    if (c.top_n > kTopnSortCap) throw Status(LP_BAD_PARAMS, "top_n above the device sort capacity");
 }
 
 // Constant per-configuration tables for the extractor.

@@ -21,6 +21,7 @@
 // All FP ops are explicit round-to-nearest (no FMA), matching the reference.
 
 #include "lorb.cuh"
+#include "prims.cuh"
 
 namespace lpb {
 
@@ -438,6 +439,11 @@ __global__ void __launch_bounds__(256, 4) k_detect9(const __grid_constant__ Extr
 }
 
 // ---------------------------------------------------------------------------
+__global__ void k_iota_int(int* p, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = i;
+}
+
 // k_topn: exact per-region select_top_n via MSB radix select + bitonic sort
 __device__ void bitonic_desc(uint64_t* v, int n_pow2) {
     for (int k = 2; k <= n_pow2; k <<= 1)
@@ -923,6 +929,44 @@ __global__ void __launch_bounds__(256) k_describe6(const __grid_constant__ Extra
     if (lane == 0) a.kp_out[static_cast<size_t>(rg.out_slot) * a.cap_slot + idx] = kp;
 }
 
+// top_n > kTopnSortCap: per region, the survivor keys (descending = the
+// reference's (response desc, y asc, x asc) order, lorb.hpp:291-299) sorted
+// by the global radix sort (prims.cuh) as two chained stable 32-bit passes
+// over the inverted key (low word, then high word); slots past the survivor
+// count carry ~0 and, being later in input order, stay behind every survivor
+__global__ void k_topn_words(ExtractArgs a, int ri, int half, const int* idx, uint32_t* words) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.surv_cap) return;
+    const int n = min(static_cast<int>(a.surv_count[ri]), a.surv_cap);
+    const int j = idx ? idx[i] : i;
+    const uint64_t k = j < n ? ~a.surv[static_cast<size_t>(ri) * a.surv_cap + j] : ~0ull;
+    words[i] = half ? static_cast<uint32_t>(k >> 32) : static_cast<uint32_t>(k);
+}
+__global__ void k_topn_emit(ExtractArgs a, int ri, const int* idx) {
+    const int n = min(static_cast<int>(a.surv_count[ri]), a.surv_cap);
+    const int out_n = min(n, a.top_n);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) a.count_region[ri] = out_n;
+    if (i >= out_n) return;
+    float r;
+    int x, y;
+    kp_unkey(a.surv[static_cast<size_t>(ri) * a.surv_cap + idx[i]], &r, &x, &y);
+    a.kp_region[static_cast<size_t>(ri) * a.top_n + i] = lp_keypoint{x, y, r, ri};
+}
+static void topn_global(const ExtractArgs& a, cudaStream_t s) {
+    const int n = a.surv_cap;
+    DBuf ka(sizeof(uint32_t) * n, s), kb(sizeof(uint32_t) * n, s), ia(sizeof(int) * n, s), ib(sizeof(int) * n, s),
+        hist(sizeof(unsigned) * 256 * cdiv(n, kPrimTile), s);
+    for (int ri = 0; ri < a.nregions; ++ri) {
+        LPB_LAUNCH(k_iota_int, cdiv(n, 256), 256, 0, s, ia.as<int>(), n);
+        LPB_LAUNCH(k_topn_words, cdiv(n, 256), 256, 0, s, a, ri, 0, static_cast<const int*>(nullptr), ka.as<uint32_t>());
+        radix_sort_pairs(ka.as<uint32_t>(), ia.as<int>(), kb.as<uint32_t>(), ib.as<int>(), n, 32, hist.as<unsigned>(), s);
+        LPB_LAUNCH(k_topn_words, cdiv(n, 256), 256, 0, s, a, ri, 1, ia.as<int>(), ka.as<uint32_t>());
+        radix_sort_pairs(ka.as<uint32_t>(), ia.as<int>(), kb.as<uint32_t>(), ib.as<int>(), n, 32, hist.as<unsigned>(), s);
+        LPB_LAUNCH(k_topn_emit, cdiv(a.top_n, 256), 256, 0, s, a, ri, ia.as<int>());
+    }
+}
+
 void extract_launch(const ExtractArgs& a, cudaStream_t s) {
     if (a.nregions == 0) return;
     LPB_CUDA(cudaMemsetAsync(a.surv_count, 0, sizeof(unsigned) * a.nregions, s));
@@ -934,6 +978,8 @@ void extract_launch(const ExtractArgs& a, cudaStream_t s) {
     }
     if (a.top_n <= kTopnRankCap) {
         LPB_LAUNCH(k_topn, a.nregions, 1024, 0, s, a);
+    } else if (a.top_n > kTopnSortCap) {
+        topn_global(a, s);
     } else {
         const int topn_smem = kTopnSortCap * sizeof(uint64_t);
         ensure_dyn_smem(reinterpret_cast<const void*>(k_topn_radix), topn_smem);

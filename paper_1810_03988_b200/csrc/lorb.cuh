@@ -16,9 +16,9 @@ struct DevRegion {
 
 constexpr int kDetTileX = 64;    // output tile of the detect kernel (columns)
 constexpr int kDetTileY = 32;    // (rows)
-constexpr int kMaxHarrisR = 6;   // harris_sigma <= 2 (radius ceil(3 sigma))
-constexpr int kMaxBlurR = 12;    // brief_blur_sigma <= 4
-constexpr int kTopnSortCap = 8192;
+constexpr int kMaxHarrisR = 12;  // harris_sigma <= 4 (radius ceil(3 sigma)); the generic tile's static smem
+constexpr int kMaxBlurR = 24;    // brief_blur_sigma <= 8
+constexpr int kTopnSortCap = 8192;  // k_topn_radix's shared sort; larger top_n: global radix sort per region
 constexpr int kDescribeFastBlurR = 6;  // k_describe6's blur radius (sigma = 2)
 constexpr int kTopnRankCap = 2048;   // k_topn fast path: rank placement of <= 2048 keys
 constexpr int kTopnHistBins = 4096;  // first radix digit: top 12 key bits

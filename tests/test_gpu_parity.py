@@ -149,6 +149,32 @@ def test_extract_top_n_paths(lp, orc, params, top_n):
     assert np.array_equal(ka, kb) and np.array_equal(da, db)
 
 
+def test_extract_widened_parameter_domain(lp, orc):
+    """ExtractionConfig::validate (lorb.hpp:82-89) accepts any sigma > 0 and
+    top_n >= 4. The device covers harris_sigma <= 4 (generic detect tile),
+    brief_blur_sigma <= 8 and any top_n (> 8192: the global radix-sort top-N
+    path); beyond the two sigma bounds it raises BadParams (tested below)."""
+    img = orc.texture(1920, 1080, 21)
+    reg = [(20, 20, 1900, 1060, 0)]
+    for hs, bs, top_n in ((3.5, 2.0, 500), (1.0, 6.0, 300), (1.0, 2.0, 9000), (2.6, 5.5, 12000)):
+        cfg = orc.default_params().extraction
+        cfg.harris_sigma, cfg.brief_blur_sigma, cfg.top_n = hs, bs, top_n
+        pat = orc.brief_pattern(cfg.n_d, cfg.patch_half, 42)
+        ka, da = lp.extract_features(img, reg, cfg, pat)
+        kb, db = orc.extract_features(img, reg, cfg, pat)
+        assert len(ka) == len(kb) > 0, (hs, bs, top_n)
+        assert np.array_equal(ka, kb), (hs, bs, top_n)
+        assert np.array_equal(da, db), (hs, bs, top_n)
+    from paper_1810_03988_b200 import abi
+    for hs, bs in ((4.2, 2.0), (1.0, 8.5)):
+        cfg = orc.default_params().extraction
+        cfg.harris_sigma, cfg.brief_blur_sigma = hs, bs
+        pat = orc.brief_pattern(cfg.n_d, cfg.patch_half, 42)
+        with pytest.raises(abi.LorbError) as e:
+            lp.extract_features(img, reg, cfg, pat)
+        assert e.value.name == "BadParams", e.value.name
+
+
 # ---------------------------------------------------------------- matching
 def _descs(orc, params, w=640, h=480):
     l, r, _ = orc.planted_pair(w, h, 0.25, 42)
