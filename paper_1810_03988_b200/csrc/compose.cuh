@@ -13,7 +13,7 @@ struct Win {
     int p;  // row pitch in elements (w rounded up to a multiple of 4: float4 rows)
 };
 
-constexpr int kMaxCompCams = 16;   // cameras per rig on the fused compositor path
+constexpr int kMaxCompCams = 32;   // cameras per rig on the fused compositor path
 constexpr int kMaxCompLevels = 12; // blend levels (canvas >= 2^11 px per side for 12)
 constexpr int kRunSlots = 4;       // coverage runs stored inline per window row
 constexpr int kBlendAlignX = 64;   // level-0 window x alignment (blend tile width at level 0)

@@ -11,11 +11,13 @@
 //    PROSAC, HomographyCache and the windowed warp / multi-band compositor all
 //    run on the GPU, and the packet's keypoints, descriptors, matches,
 //    homographies and composite come back with the frame
-//    (lp_rig_submit_frame / lp_rig_wait_frame). Pipelined mode keeps up to
+//    (lp_rig_submit_frame / lp_rig_wait_frame). Pipelined mode runs an ingest
+//    thread and an output (sink) thread around a device loop that keeps up to
 //    min(frames_in_flight, 3) frames on the device at once (the rig's frame
-//    slots) instead of one host thread per stage; Serial keeps one. Both
-//    deliver the same packets in frame order, so composites are
-//    byte-identical between the modes as in the reference.
+//    slots) instead of one host thread per stage; Serial runs one frame at a
+//    time on the calling thread. Both deliver the same packets in frame
+//    order, so composites are byte-identical between the modes as in the
+//    reference.
 //  * The stage bodies (stage_rectify_crop ... stage_warp_blend) stay callable
 //    on their own, as in the reference, and run on the device through the
 //    drop-in primitives; stage_describe blurs each region once and describes
@@ -44,7 +46,9 @@
 #include <memory>
 #include <mutex>
 #include <optional>
+#include <exception>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "lorbpano/b200_runtime.hpp"
@@ -318,6 +322,41 @@ using FrameSource = std::function<std::optional<std::vector<ImageU8>>()>;
 using FrameSink = std::function<void(const FramePacket&)>;
 
 namespace detail {
+// A bounded FIFO between the engine's threads; close() releases the waiters.
+template <class T>
+class Channel {
+public:
+    explicit Channel(std::size_t cap) : cap_(std::max<std::size_t>(cap, 1)) {}
+    void put(T v) {
+        std::unique_lock<std::mutex> l(mu_);
+        room_.wait(l, [&] { return q_.size() < cap_ || shut_; });
+        q_.push_back(std::move(v));
+        ready_.notify_one();
+    }
+    std::optional<T> take() {
+        std::unique_lock<std::mutex> l(mu_);
+        ready_.wait(l, [&] { return !q_.empty() || shut_; });
+        if (q_.empty()) return std::nullopt;
+        T v = std::move(q_.front());
+        q_.pop_front();
+        room_.notify_one();
+        return v;
+    }
+    void close() {
+        std::lock_guard<std::mutex> l(mu_);
+        shut_ = true;
+        ready_.notify_all();
+        room_.notify_all();
+    }
+
+private:
+    std::size_t cap_;
+    std::deque<T> q_;
+    bool shut_ = false;
+    std::mutex mu_;
+    std::condition_variable ready_, room_;
+};
+
 inline std::int64_t now_ns() {
     return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
         .count();
@@ -358,28 +397,10 @@ public:
     Metrics run(const FrameSource& source, const FrameSink& sink) {
         Metrics m;
         const auto start = std::chrono::steady_clock::now();
-        // frames on the device at once: the rig has 3 frame slots
-        const std::size_t depth =
-            cfg_.mode == PipelineMode::Serial ? 1 : static_cast<std::size_t>(std::clamp(cfg_.frames_in_flight, 1, 3));
-        std::deque<Flight*> inflight;
-        std::uint64_t index = 0, launched = 0;
-        for (;;) {
-            std::unique_ptr<FramePacket> pkt = ingest(source, index, m);
-            if (!pkt) break;
-            note_warmup(index + 1);
-            ++index;
-            Flight& f = flights_[launched++ % flights_.size()];
-            launch(f, std::move(pkt), m);
-            inflight.push_back(&f);
-            while (inflight.size() >= depth) {
-                land(*inflight.front(), m, sink);
-                inflight.pop_front();
-            }
-        }
-        while (!inflight.empty()) {
-            land(*inflight.front(), m, sink);
-            inflight.pop_front();
-        }
+        if (cfg_.mode == PipelineMode::Serial)
+            run_serial(source, sink, m);
+        else
+            run_pipelined(source, sink, m);
         m.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
         m.frames_per_second = m.wall_seconds > 0 ? m.frames_out / m.wall_seconds : 0.0;
         if (pool_) {
@@ -613,11 +634,17 @@ private:
         }
     }
 
-    static void note_drop(FramePacket& pkt, Stage s, const std::string& why, Metrics& m) {
+    void note_drop(FramePacket& pkt, Stage s, const std::string& why, Metrics& m) {
         pkt.failed = true;
         pkt.fail_stage = s;
         pkt.fail_reason = why;
+        std::lock_guard<std::mutex> l(metrics_mu_);
         m.drops.push_back(DroppedFrame{pkt.frame_index, s, why});
+    }
+    // the engine's threads share one Metrics
+    void note_stage(Metrics& m, Stage s, double ns) {
+        std::lock_guard<std::mutex> l(metrics_mu_);
+        m.stage_ns[static_cast<int>(s)].push_back(ns);
     }
 
     void note_warmup(std::uint64_t started) {
@@ -650,8 +677,11 @@ private:
             dst.data.assign(src.data.begin(), src.data.end());
         }
         span.end_ns = detail::now_ns();
-        m.stage_ns[static_cast<int>(Stage::Ingest)].push_back(static_cast<double>(span.end_ns - span.start_ns));
-        ++m.frames_in;
+        note_stage(m, Stage::Ingest, static_cast<double>(span.end_ns - span.start_ns));
+        {
+            std::lock_guard<std::mutex> l(metrics_mu_);
+            ++m.frames_in;
+        }
         return pkt;
     }
 
@@ -669,7 +699,7 @@ private:
             return false;
         }
         span.end_ns = detail::now_ns();
-        m.stage_ns[static_cast<int>(s)].push_back(static_cast<double>(span.end_ns - span.start_ns));
+        note_stage(m, s, static_cast<double>(span.end_ns - span.start_ns));
         return true;
     }
 
@@ -679,7 +709,8 @@ private:
         if (!pkt->failed) {
             sink(*pkt);
             span.end_ns = detail::now_ns();
-            m.stage_ns[static_cast<int>(Stage::Output)].push_back(static_cast<double>(span.end_ns - span.start_ns));
+            note_stage(m, Stage::Output, static_cast<double>(span.end_ns - span.start_ns));
+            std::lock_guard<std::mutex> l(metrics_mu_);
             ++m.frames_out;
         }
         pool_->release(std::move(pkt));
@@ -727,6 +758,79 @@ private:
 
     // rectify/crop + regions on the host-visible path, then the frame to the
     // device rig; a frame the rig cannot take runs the stage bodies here
+    // one frame at a time on the calling thread (frames_in_flight 1)
+    void run_serial(const FrameSource& source, const FrameSink& sink, Metrics& m) {
+        for (std::uint64_t index = 0;; ++index) {
+            std::unique_ptr<FramePacket> pkt = ingest(source, index, m);
+            if (!pkt) break;
+            note_warmup(index + 1);
+            Flight& f = flights_[0];
+            launch(f, std::move(pkt), m);
+            deliver(land(f, m), m, sink);
+        }
+    }
+
+    // Pipelined (pipeline.hpp:660-711 as threads + device slots): an ingest
+    // thread pulls frames into pooled packets, the calling thread keeps up to
+    // min(frames_in_flight, 3) of them on the device, an output thread runs
+    // the sink; frames leave in order
+    void run_pipelined(const FrameSource& source, const FrameSink& sink, Metrics& m) {
+        const std::size_t depth = static_cast<std::size_t>(std::clamp(cfg_.frames_in_flight, 1, 3));
+        const std::size_t qcap = static_cast<std::size_t>(std::max(cfg_.frames_in_flight, 1));
+        detail::Channel<std::unique_ptr<FramePacket>> in(qcap), out(qcap);
+        std::exception_ptr ingest_error, sink_error;
+        std::thread ingest_thread([&] {
+            try {
+                for (std::uint64_t index = 0;; ++index) {
+                    std::unique_ptr<FramePacket> pkt = ingest(source, index, m);
+                    if (!pkt) break;
+                    note_warmup(index + 1);
+                    in.put(std::move(pkt));
+                }
+            } catch (...) {
+                ingest_error = std::current_exception();
+            }
+            in.close();
+        });
+        std::thread output_thread([&] {
+            for (;;) {
+                std::optional<std::unique_ptr<FramePacket>> pkt = out.take();
+                if (!pkt) break;
+                if (sink_error) {  // keep draining so the packets return to the pool
+                    pool_->release(std::move(*pkt));
+                    continue;
+                }
+                try {
+                    deliver(std::move(*pkt), m, sink);
+                } catch (...) {
+                    sink_error = std::current_exception();
+                }
+            }
+        });
+        std::deque<Flight*> inflight;
+        std::uint64_t launched = 0;
+        for (;;) {
+            std::optional<std::unique_ptr<FramePacket>> pkt = in.take();
+            if (!pkt) break;
+            Flight& f = flights_[launched++ % flights_.size()];
+            launch(f, std::move(*pkt), m);
+            inflight.push_back(&f);
+            while (inflight.size() >= depth) {
+                out.put(land(*inflight.front(), m));
+                inflight.pop_front();
+            }
+        }
+        while (!inflight.empty()) {
+            out.put(land(*inflight.front(), m));
+            inflight.pop_front();
+        }
+        out.close();
+        ingest_thread.join();
+        output_thread.join();
+        if (ingest_error) std::rethrow_exception(ingest_error);
+        if (sink_error) std::rethrow_exception(sink_error);
+    }
+
     void launch(Flight& f, std::unique_ptr<FramePacket> pkt, Metrics& m) {
         FramePacket& p = *pkt;
         f.pkt = std::move(pkt);
@@ -783,7 +887,7 @@ private:
     }
 
     // the frame back from the device into its packet, then to the sink
-    void land(Flight& f, Metrics& m, const FrameSink& sink) {
+    std::unique_ptr<FramePacket> land(Flight& f, Metrics& m) {
         FramePacket& p = *f.pkt;
         if (f.ticket != 0 && !p.failed) {
             const lp_status st = lp_rig_wait_frame(rig_, f.ticket, &f.out);
@@ -793,7 +897,7 @@ private:
                 fill_packet(f, m);
             }
         }
-        deliver(std::move(f.pkt), m, sink);
+        return std::move(f.pkt);
     }
 
     void fill_packet(Flight& f, Metrics& m) {
@@ -840,7 +944,7 @@ private:
             span.start_ns = t;
             t += static_cast<std::int64_t>(dev[i] * ms_to_ns);
             span.end_ns = t;
-            m.stage_ns[static_cast<int>(stages[i])].push_back(dev[i] * ms_to_ns);
+            note_stage(m, stages[i], dev[i] * ms_to_ns);
         }
     }
 
@@ -855,6 +959,7 @@ private:
     lp_rig* rig_ = nullptr;
     int rig_cams_ = 0, rig_w_ = 0, rig_h_ = 0;
     std::array<Flight, 3> flights_;
+    std::mutex metrics_mu_;
 };
 
 /// A pool sized for `frames_in_flight` packets (pipeline.hpp:724-735).
