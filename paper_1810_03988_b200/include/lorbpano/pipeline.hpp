@@ -40,6 +40,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <functional>
@@ -397,8 +398,13 @@ public:
     Metrics run(const FrameSource& source, const FrameSink& sink) {
         Metrics m;
         const auto start = std::chrono::steady_clock::now();
+        // LPB_ENGINE_THREADS=0: Pipelined without the ingest / sink threads
+        // (A/B experiments; the default is the measured best)
+        const char* thr = std::getenv("LPB_ENGINE_THREADS");
         if (cfg_.mode == PipelineMode::Serial)
-            run_serial(source, sink, m);
+            run_serial(source, sink, m, 1);
+        else if (thr && thr[0] == '0')
+            run_serial(source, sink, m, device_depth());
         else
             run_pipelined(source, sink, m);
         m.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
@@ -758,16 +764,32 @@ private:
 
     // rectify/crop + regions on the host-visible path, then the frame to the
     // device rig; a frame the rig cannot take runs the stage bodies here
-    // one frame at a time on the calling thread (frames_in_flight 1)
-    void run_serial(const FrameSource& source, const FrameSink& sink, Metrics& m) {
+    // frames on the device at once: the rig has 3 frame slots; one pool
+    // packet stays free for the host stages (LPB_ENGINE_DEPTH overrides)
+    std::size_t device_depth() const {
+        int d = std::min(cfg_.frames_in_flight - 1, 3);
+        if (const char* e = std::getenv("LPB_ENGINE_DEPTH")) d = std::atoi(e);
+        return static_cast<std::size_t>(std::clamp(d, 1, 3));
+    }
+
+    // the calling thread alone: ingest, device (up to `depth` frames in
+    // flight), sink; Serial mode is depth 1
+    void run_serial(const FrameSource& source, const FrameSink& sink, Metrics& m, std::size_t depth) {
+        std::deque<Flight*> inflight;
+        std::uint64_t launched = 0;
         for (std::uint64_t index = 0;; ++index) {
             std::unique_ptr<FramePacket> pkt = ingest(source, index, m);
             if (!pkt) break;
             note_warmup(index + 1);
-            Flight& f = flights_[0];
+            Flight& f = flights_[launched++ % flights_.size()];
             launch(f, std::move(pkt), m);
-            deliver(land(f, m), m, sink);
+            inflight.push_back(&f);
+            while (inflight.size() >= depth) {
+                deliver(land(*inflight.front(), m), m, sink);
+                inflight.pop_front();
+            }
         }
+        for (Flight* f : inflight) deliver(land(*f, m), m, sink);
     }
 
     // Pipelined (pipeline.hpp:660-711 as threads + device slots): an ingest
@@ -775,7 +797,7 @@ private:
     // min(frames_in_flight, 3) of them on the device, an output thread runs
     // the sink; frames leave in order
     void run_pipelined(const FrameSource& source, const FrameSink& sink, Metrics& m) {
-        const std::size_t depth = static_cast<std::size_t>(std::clamp(cfg_.frames_in_flight, 1, 3));
+        const std::size_t depth = device_depth();
         const std::size_t qcap = static_cast<std::size_t>(std::max(cfg_.frames_in_flight, 1));
         detail::Channel<std::unique_ptr<FramePacket>> in(qcap), out(qcap);
         std::exception_ptr ingest_error, sink_error;
