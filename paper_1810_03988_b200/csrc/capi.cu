@@ -51,21 +51,6 @@ static int graph_kernel_nodes(cudaGraph_t g) {
     return k;
 }
 // the kernel node of a captured graph that launches `fn` (first one), or null
-static cudaGraphNode_t find_kernel_node(cudaGraph_t g, const void* fn) {
-    if (!g) return nullptr;
-    size_t n = 0;
-    if (cudaGraphGetNodes(g, nullptr, &n) != cudaSuccess) return nullptr;
-    std::vector<cudaGraphNode_t> nodes(n);
-    if (n && cudaGraphGetNodes(g, nodes.data(), &n) != cudaSuccess) return nullptr;
-    for (auto nd : nodes) {
-        cudaGraphNodeType t;
-        if (cudaGraphNodeGetType(nd, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
-        cudaKernelNodeParams kp;
-        if (cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess && kp.func == fn) return nd;
-    }
-    cudaGetLastError();
-    return nullptr;
-}
 static thread_local std::string g_err;
 
 // ---- kernel profiler: events around every launch, keyed "name/occurrence"

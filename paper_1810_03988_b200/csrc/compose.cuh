@@ -46,6 +46,149 @@ __host__ __device__ constexpr int lean_cx(int txk) { return (txk / 2 + 3 + 3 + 3
 // box bw x bh, zero fill out of bounds). False if the driver refuses.
 bool tma_encode_f32_2d(CUtensorMap* m, const float* base, int w, int h, int pitch, int bw, int bh);
 
+// ---- compositor geometry of one homography set (host and device) ----
+// canvas (compute_canvas, compose.hpp:32-68), blend levels
+// (pipeline.hpp:511-514, gaussian_pyramid's size check), each camera's
+// level-0 window = projected-corner bbox + (4 * 2^L + 8) px, y aligned to
+// 2^(L-1), x to max(2^(L-1), 64), and the inverse maps
+// (Homography::inverse, homography.hpp:36-48). One function for the host
+// (prepare_compositor) and the device (k_geom), so both derive the same
+// integers from the same doubles.
+struct RigGeom {
+    int cw, ch, ox, oy;  // canvas width, height, origin
+    int levels;
+    Win win0[kMaxCompCams];
+};
+
+__host__ __device__ inline double geom_det(const double* h) {
+    return h[0] * (h[4] * h[8] - h[5] * h[7]) - h[1] * (h[3] * h[8] - h[5] * h[6]) + h[2] * (h[3] * h[7] - h[4] * h[6]);
+}
+
+// 0 on success, else the lp_status the reference would throw
+__host__ __device__ inline int rig_geometry(int ncams, int w, int h, int blend_levels, const lp_homography* H,
+                                            RigGeom* g, double* hinv) {
+    double minx = 1.7976931348623157e308, miny = minx, maxx = -minx, maxy = -minx;
+    for (int c = 0; c < ncams; ++c) {
+        const double* m = H[c].h;
+        if (fabs(geom_det(m)) < 1e-9) return LP_SINGULAR_HOMOGRAPHY;
+        const double cs[4][2] = {{0, 0}, {static_cast<double>(w), 0}, {0, static_cast<double>(h)},
+                                 {static_cast<double>(w), static_cast<double>(h)}};
+        for (int q = 0; q < 4; ++q) {
+            const double wd = m[6] * cs[q][0] + m[7] * cs[q][1] + m[8];
+            const double x = (m[0] * cs[q][0] + m[1] * cs[q][1] + m[2]) / wd;
+            const double y = (m[3] * cs[q][0] + m[4] * cs[q][1] + m[5]) / wd;
+            minx = fmin(minx, x);
+            miny = fmin(miny, y);
+            maxx = fmax(maxx, x);
+            maxy = fmax(maxy, y);
+        }
+    }
+    g->ox = static_cast<int>(floor(minx));
+    g->oy = static_cast<int>(floor(miny));
+    g->cw = static_cast<int>(ceil(maxx)) - g->ox;
+    g->ch = static_cast<int>(ceil(maxy)) - g->oy;
+    int levels = blend_levels;
+    while (levels > 1 && (g->cw < (1 << (levels - 1)) || g->ch < (1 << (levels - 1)))) --levels;
+    if (levels < 1 || levels > kMaxCompLevels) return LP_TOO_MANY_LEVELS;
+    {
+        int ww = g->cw, hh = g->ch;
+        for (int i = 1; i < levels; ++i) {
+            if (ww < 2 || hh < 2) return LP_TOO_MANY_LEVELS;
+            ww /= 2;
+            hh /= 2;
+        }
+    }
+    g->levels = levels;
+    const int align = 1 << (levels - 1);
+    const int align_x = align > kBlendAlignX ? align : kBlendAlignX;
+    const int margin = 4 * (1 << levels) + 8;
+    for (int c = 0; c < ncams; ++c) {
+        const double* m = H[c].h;
+        const double d = geom_det(m);
+        double inv[9] = {(m[4] * m[8] - m[5] * m[7]) / d, (m[2] * m[7] - m[1] * m[8]) / d,
+                         (m[1] * m[5] - m[2] * m[4]) / d, (m[5] * m[6] - m[3] * m[8]) / d,
+                         (m[0] * m[8] - m[2] * m[6]) / d, (m[2] * m[3] - m[0] * m[5]) / d,
+                         (m[3] * m[7] - m[4] * m[6]) / d, (m[1] * m[6] - m[0] * m[7]) / d,
+                         (m[0] * m[4] - m[1] * m[3]) / d};
+        const double i8 = inv[8];
+        for (int j = 0; j < 9; ++j) hinv[9 * c + j] = fabs(i8) > 1e-12 ? inv[j] / i8 : inv[j];
+        double mnx = 1.7976931348623157e308, mny = mnx, mxx = -mnx, mxy = -mnx;
+        bool behind = false;
+        const double cs[4][2] = {{0, 0}, {static_cast<double>(w), 0}, {0, static_cast<double>(h)},
+                                 {static_cast<double>(w), static_cast<double>(h)}};
+        for (int q = 0; q < 4; ++q) {
+            if (m[6] * cs[q][0] + m[7] * cs[q][1] + m[8] <= 0) behind = true;
+            const double wd = m[6] * cs[q][0] + m[7] * cs[q][1] + m[8];
+            const double x = (m[0] * cs[q][0] + m[1] * cs[q][1] + m[2]) / wd;
+            const double y = (m[3] * cs[q][0] + m[4] * cs[q][1] + m[5]) / wd;
+            mnx = fmin(mnx, x);
+            mny = fmin(mny, y);
+            mxx = fmax(mxx, x);
+            mxy = fmax(mxy, y);
+        }
+        Win wv{0, 0, 0, 0, 0};
+        if (behind) {
+            wv = Win{0, 0, (g->cw + align_x - 1) / align_x * align_x, g->ch, 0};
+        } else {
+            long long x0 = static_cast<long long>(floor(mnx)) - g->ox - margin;
+            long long y0 = static_cast<long long>(floor(mny)) - g->oy - margin;
+            long long x1 = static_cast<long long>(ceil(mxx)) - g->ox + margin;
+            long long y1 = static_cast<long long>(ceil(mxy)) - g->oy + margin;
+            x0 = x0 > 0 ? (x0 / align_x) * align_x : 0;
+            y0 = y0 > 0 ? (y0 / align) * align : 0;
+            const long long xcap = (g->cw + align_x - 1) / align_x * align_x;
+            const long long xr = (x1 + align_x - 1) / align_x * align_x;
+            x1 = xr < xcap ? xr : xcap;
+            y1 = y1 < g->ch ? y1 : g->ch;
+            wv = Win{static_cast<int>(x0), static_cast<int>(y0), static_cast<int>(x1 - x0 > 0 ? x1 - x0 : 0),
+                     static_cast<int>(y1 - y0 > 0 ? y1 - y0 : 0), 0};
+        }
+        g->win0[c] = wv;
+    }
+    for (int c = ncams; c < kMaxCompCams; ++c) g->win0[c] = Win{0, 0, 0, 0, 0};
+    return 0;
+}
+
+__host__ __device__ inline bool same_geometry(const RigGeom& a, const RigGeom& b, int ncams) {
+    if (a.cw != b.cw || a.ch != b.ch || a.ox != b.ox || a.oy != b.oy || a.levels != b.levels) return false;
+    for (int c = 0; c < ncams; ++c)
+        if (a.win0[c].x0 != b.win0[c].x0 || a.win0[c].y0 != b.win0[c].y0 || a.win0[c].w != b.win0[c].w ||
+            a.win0[c].h != b.win0[c].h)
+            return false;
+    return true;
+}
+
+// ---- inverse maps in __constant__ memory: k_warp reads camera c's map as
+// constant-bank operands from c_hinv[hinv_base + c]; the rig updates them by
+// stream-ordered copies (from the host after a host-side estimate, or from
+// the device after k_geom), so no launch parameters change per frame
+constexpr int kConstHinvSlots = 896;  // cameras of all live rigs (64 KB constant bank)
+int hinv_slots_alloc(int n);           // first of n consecutive slots (throws CapacityOverflow)
+void hinv_slots_free(int base, int n);
+void hinv_upload(int base, const double* src, int n, bool src_on_device, cudaStream_t s);
+
+// ---- k_geom: the estimator's verdict on the device (HomographyCache,
+// pipeline.hpp:259-286) for a re-registering frame that does not synchronise
+// the host: the new chain if the estimate succeeded, else the cached one;
+// its inverse maps; whether its geometry equals the one the compositor
+// arenas were built for. The record lands in host-mapped memory.
+struct GeomOutcome {
+    unsigned long long ticket;
+    int done, estimated, same, status;
+    lp_homography H[kMaxCompCams];
+};
+struct GeomArgs {
+    int ncams, w, h, blend_levels;
+    const lp_homography* chain;
+    const int* chain_status;
+    lp_homography* cached;  // device copy of the cache, updated on success
+    const RigGeom* ref;     // geometry of the compositor arenas
+    double* hinv;           // 9 * ncams, written only when the geometry could be derived
+    GeomOutcome* out;       // host-mapped
+    unsigned long long ticket;
+};
+void geom_launch(const GeomArgs& a, cudaStream_t s);
+
 // Passed by value (constant bank): all per-camera geometry and pointers.
 struct ComposeArgs {
     int ncams, levels;
@@ -68,7 +211,7 @@ struct ComposeArgs {
     int Rp[kMaxCompLevels];                    // their row pitch (W[k] rounded up to 4)
     float down_taps[7];                        // gaussian_kernel(1.0f)
     DevImage src[kMaxCompCams];                // u8 grayscale cameras
-    double hinv[kMaxCompCams][9];
+    int hinv_base;                             // camera c's inverse map: c_hinv[hinv_base + c]
     uint8_t* out;                              // W[0] x H[0]
     int* status;
     // host pointer (never read on the device): PyrTma per source level k,
@@ -90,7 +233,6 @@ void rectify_launch(const RectCam* cams, int ncams, int in_w, int in_h, int max_
 
 // Full per-frame compositor: warp, coverage runs, pyramids, band blend + collapse.
 void compose_launch(const ComposeArgs& a, cudaStream_t s);
-const void* warp_kernel_fn();  // k_warp, for patching its node in a captured chain
 // Pyramid + blend + collapse only (level-0 images and masks already in G/M).
 void blend_launch(const ComposeArgs& a, cudaStream_t s);
 

@@ -511,6 +511,39 @@ def test_rig_frames_in_flight_with_details(lp, orc):
         assert g["stage_ms"][3] > 0
 
 
+@pytest.mark.parametrize("in_flight", [1, 3])
+def test_async_reregistration_geometry_changes(lp, orc, in_flight):
+    """Once a homography set is cached, a refresh frame's verdict, inverse maps
+    and geometry check come from the device (k_geom) and the host harvests
+    them later. Frames here alternate between two planted overlaps, so the
+    canvas and the windows move between frames and the host must compose
+    those frames again on their own geometry (repair), with up to 3 frames
+    in flight; every panorama, homography and match list equals the
+    oracle's for that frame."""
+    from paper_1810_03988_b200 import Rig
+    p = orc.default_params()
+    p.seed = p.matching.seed = 42
+    p.homography_refresh = 1
+    overlaps = [0.25, 0.35, 0.35, 0.25, 0.30, 0.30, 0.25]
+    frames = [orc.planted_pair(480, 270, ov, 7)[:2] for ov in overlaps]
+    rig = Rig(lp, 2, 480, 270, p)
+    got, inflight = {}, []
+    for t, (l, r) in enumerate(frames):
+        inflight.append((t, rig.submit_frame([l, r], t)))
+        if len(inflight) >= in_flight:
+            t0, hnd = inflight.pop(0)
+            got[t0] = rig.wait_frame(hnd)
+    for t0, hnd in inflight:
+        got[t0] = rig.wait_frame(hnd)
+    for t, (l, r) in enumerate(frames):
+        want = orc.stitch_frame([l, r], p, frame_index=t)
+        g = got[t]
+        assert g["canvas"] == want["canvas"], (t, g["canvas"], want["canvas"])
+        assert np.array_equal(g["homographies"], want["homographies"]), t
+        assert np.array_equal(g["matches"][0], want["matches"][0]), t
+        assert np.array_equal(g["panorama"], want["panorama"]), t
+
+
 def test_concurrent_rigs_threads(lp, orc):
     """Independent rigs on one context, driven from host threads (the config-5
     shape): each rig has its own stage stream, so their frames overlap on the
