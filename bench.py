@@ -52,38 +52,47 @@ CONFIGS = {
 
 def run_streams(args, cfgd, lp, world, rank, local, dist):
     """Config 5: the rank's contiguous share of 64 independent 2-camera streams
-    (one rig each), driven by host threads so the rigs' per-frame estimator
-    synchronisations overlap. A step = one frame of every stream of the job."""
+    (one rig each), driven by host threads, each keeping up to LPB_CFG5_DEPTH
+    frames of each of its rigs in flight. A step = one frame of every stream
+    of the job."""
     import threading
 
     import torch
 
-    from paper_1810_03988_b200 import Rig, kernel_launches
+    from paper_1810_03988_b200 import Rig, kernel_launches, load
     from paper_1810_03988_b200.shard import RankResult, aggregate_fps, gather_results, shard_streams
+    lib = load()
     mine = shard_streams(cfgd["streams"], world, rank)
     p = lp.default_params()
     p.seed = p.matching.seed = 42
     p.homography_refresh = cfgd["refresh"]
     w, h = cfgd["w"], cfgd["h"]
-    rigs, inputs, panos = [], [], []
+    rigs, host_in, inputs, panos = [], [], [], []
     for s in mine:
         sets, _ = make_frame_sets(2, w, h, 1, seed=42 + s)
+        host_in.append(sets[0])
         inputs.append([torch.from_numpy(c).cuda() for c in sets[0]])
         rig = Rig(lp, 2, w, h, p)
         rigs.append(rig)
         panos.append(torch.empty(rig.panorama_capacity(), dtype=torch.uint8, device="cuda"))
     nthreads = min(len(rigs), int(os.environ.get("LPB_CFG5_THREADS", "32")))
+    depth = int(os.environ.get("LPB_CFG5_DEPTH", "2"))
     groups = [list(range(i, len(rigs), nthreads)) for i in range(nthreads)]
 
-    def run(steps, base):
+    def run(steps, base, ins, outs):
         errs = []
 
         def worker(ids):
             try:
+                pending = {i: [] for i in ids}
                 for t in range(steps):
                     for i in ids:
-                        tk = rigs[i].submit([x.data_ptr() for x in inputs[i]], base + t,
-                                            panos[i].data_ptr(), panos[i].numel())
+                        pending[i].append(rigs[i].submit([x.data_ptr() for x in ins[i]], base + t,
+                                                         outs[i][t % len(outs[i])].data_ptr(), outs[i][0].numel()))
+                        if len(pending[i]) >= depth:
+                            rigs[i].wait(pending[i].pop(0))
+                for i in ids:
+                    for tk in pending[i]:
                         rigs[i].wait(tk)
             except Exception as e:  # surfaced after join
                 errs.append(e)
@@ -95,7 +104,8 @@ def run_streams(args, cfgd, lp, world, rank, local, dist):
         if errs:
             raise errs[0]
 
-    run(args.warmup, 0)
+    dev_out = [[pb] + [torch.empty_like(pb) for _ in range(depth - 1)] for pb in panos]
+    run(args.warmup, 0, inputs, dev_out)
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
@@ -103,7 +113,7 @@ def run_streams(args, cfgd, lp, world, rank, local, dist):
     n0 = kernel_launches()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    run(args.steps, 1000)
+    run(args.steps, 1000, inputs, dev_out)
     torch.cuda.synchronize()
     el_ms = (time.perf_counter() - t0) * 1e3
     clk = clocks.stop()
@@ -111,6 +121,52 @@ def run_streams(args, cfgd, lp, world, rank, local, dist):
     csum = sum(int(pb[:1 << 20].to(torch.int64).sum().item()) for pb in panos)
     coll_dev = torch.device("cuda", local) if dist is None or dist.get_backend() == "nccl" else torch.device("cpu")
     ms_max, frames, checksums = gather_results(RankResult(args.steps * len(rigs), el_ms, csum), coll_dev)
+
+    # per-kernel roofline of one of the streams (device-resident frames)
+    roofline, stage, stage_ms = (None, {}, None)
+    if not args.no_profile:
+        fo_cap = rigs[0].panorama_capacity()
+        from paper_1810_03988_b200 import frame_out
+        fo = frame_out(panos[0].data_ptr(), fo_cap)
+        roofline, stage, stage_ms = profile_pass(
+            lib, rigs[0], lambda i: rigs[0].stitch_raw([x.data_ptr() for x in inputs[0]], 20_000 + i, fo),
+            args.steps, args.config)
+
+    # end to end: pinned host frames in, pinned host panoramas out
+    e2e = None
+    if not args.no_e2e:
+        pin_in = [[torch.from_numpy(c).pin_memory() for c in fr] for fr in host_in]
+        pin_out = [[torch.empty(pb.numel(), dtype=torch.uint8).pin_memory() for _ in range(depth)] for pb in panos]
+        run(2, 40_000, pin_in, pin_out)
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        run(args.steps, 50_000, pin_in, pin_out)
+        el = time.perf_counter() - t0
+        tt = torch.tensor([el], dtype=torch.float64, device=coll_dev)
+        if dist is not None:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": cfgd["streams"] * args.steps / float(tt.item()), "unit": "frames/s",
+               "h2d_bytes_per_step": cfgd["streams"] * 2 * w * h,
+               "d2h_bytes_per_step": None,
+               "timing": f"wall clock, {nthreads} host threads, {depth} frames in flight per stream, pinned "
+                         "host frames in and pinned host panoramas out, max over ranks"}
+        cv = rigs[0].wait(rigs[0].submit([x.data_ptr() for x in pin_in[0]], 60_000, pin_out[0][0].data_ptr(),
+                                         pin_out[0][0].numel()))
+        e2e["d2h_bytes_per_step"] = cfgd["streams"] * cv[0] * cv[1]
+
+    def params_fn(o):
+        q = o.default_params()
+        q.seed = q.matching.seed = 42
+        q.homography_refresh = cfgd["refresh"]
+        return q
+    cpu, parity = None, None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu, _ = cpu_baseline(host_in[0], params_fn, 1)
+        cpu["sample"] = "stream 0: " + cpu["sample"]
+    if rank == 0 and world == 1:
+        parity = parity_check(rigs[0], host_in[0], params_fn)
+
     if rank == 0:
         line = {"metric": METRIC, "value": aggregate_fps(frames, ms_max), "unit": "frames/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -118,12 +174,14 @@ def run_streams(args, cfgd, lp, world, rank, local, dist):
                 "vs_baseline": None, "dtype": "u8/f32/f64", "data": "synthetic",
                 "config": {"workload": cfgd["workload"], "streams": cfgd["streams"],
                            "streams_per_gpu": len(mine), "host_threads_per_gpu": nthreads,
+                           "frames_in_flight_per_stream": depth,
                            "cameras": 2, "width": w, "height": h,
                            "l2": "64 distinct streams (265 MB of frames) > 126 MB L2",
                            "parallelism": f"shards x{world} (contiguous stream blocks, no data-path collective)"},
                 "timing": "wall clock between device-wide synchronisations, max over ranks",
                 "gpu_launches": int(launches), "clocks": clk, "rank_checksums": checksums,
-                "roofline": None, "cpu_baseline": None, "e2e": None}
+                "roofline": roofline, "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
+                "stage_ms": stage_ms, "kernel_ms": stage}
         s = json.dumps(line)
         print(s)
         if args.out:
@@ -337,6 +395,83 @@ def kernel_roofline(lib, rig, key, avg_ms, launches):
             "frac_by_pipe": {p: round(f, 4) for p, f in fr.items()}}
 
 
+def profile_pass(lib, rig, step, steps, config):
+    """Per-kernel device times of `steps` frames with the rig's stages
+    serialised on one stream (concurrent extraction would otherwise inflate
+    the compositor's kernels), every kernel set against its pipes
+    (kernel_roofline), the dominant one as the line's roofline."""
+    import torch
+    lib.lp_rig_set_streams(rig.rig, 1)
+    lib.lp_profile_reset()
+    lib.lp_rig_work_reset(rig.rig)
+    lib.lp_profile_enable(1)
+    for i in range(steps):
+        step(i)
+    torch.cuda.synchronize()
+    cap = 256
+    names = C.create_string_buffer(cap * 64)
+    tot = (C.c_double * cap)()
+    cnt = (C.c_longlong * cap)()
+    lib.lp_profile_read.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
+    n = lib.lp_profile_read(names, 64, tot, cnt, cap)
+    lib.lp_profile_enable(0)
+    lib.lp_rig_set_streams(rig.rig, 2)
+    kern = {}
+    for i in range(min(n, cap)):
+        key = names.raw[i * 64:(i + 1) * 64].split(b"\0")[0].decode()
+        kern[key] = (tot[i], cnt[i])
+    step_ms = sum(v[0] for v in kern.values()) / steps
+    dom = max(kern, key=lambda k: kern[k][0])
+    # every kernel against the pipe its exact arithmetic needs most of
+    # (lp_rig_algorithmic_work: compulsory bytes, FP64 add/mul/compare,
+    # FP64 div/sqrt, FP32, POPC); the bound is the pipe with the largest
+    # fraction of its measured peak
+    per_kernel = {k: kernel_roofline(lib, rig.rig, k, kern[k][0] / kern[k][1], kern[k][1]) for k in kern}
+    # DRAM bytes of the same launch from the committed ncu --set full capture
+    # (scripts/ncu_traffic.py -> profiles/ncu_traffic.json), or null
+    traffic, limiter = None, None
+    try:
+        nj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = nj.get(config, {}).get(dom, {}).get("traffic_bytes")
+        limiter = nj.get(config, {}).get(dom, {}).get("limiter")
+    except Exception:
+        pass
+    roofline = dict(per_kernel[dom])
+    roofline.update({"kernel": dom, "traffic": traffic,
+                     # what ncu says bounds it (same capture): issue slots / FP64 pipe / DRAM
+                     "ncu_limiter": limiter,
+                     "share_of_kernel_time": kern[dom][0] / max(1e-9, sum(v[0] for v in kern.values())),
+                     "kernels": {k: {"ms": round(v["avg_launch_ms"], 4), "bound": v["bound"],
+                                     "frac": None if v["frac"] is None else round(v["frac"], 4)}
+                                 for k, v in sorted(per_kernel.items(), key=lambda kv: -kern[kv[0]][0])}})
+    stage = {k: round(v[0] / v[1], 4) for k, v in sorted(kern.items(), key=lambda kv: -kv[1][0])}
+    stage["_kernel_ms_per_frame"] = round(step_ms, 4)
+    # the reference's stages (pipeline.hpp:26-34), device ms per frame
+    ref_stages = {"rectify_crop": ("k_rectify",), "detect": ("k_detect", "k_topn"),
+                  "describe": ("k_describe",),
+                  "match_estimate": ("k_lsh_keys", "k_match_query", "k_match_finalize", "k_prosac", "k_chain"),
+                  "warp_blend": ("k_warp", "k_runs", "k_mask0", "k_pyr_down", "k_blend_level")}
+    stage_ms = {name: round(sum(v[0] for k, v in kern.items() if k.split("/")[0] in ks) / steps, 4)
+                for name, ks in ref_stages.items()}
+    return roofline, stage, stage_ms
+
+
+def parity_check(rig, frames, params_fn):
+    """The GPU rig's panorama of `frames` at frame 0 (an estimating frame, as
+    the reference engine's first) against the reference StitchEngine's."""
+    import oracle
+    if not oracle.ref_available():
+        return None
+    from oracle import Oracle
+    o = Oracle("ref")
+    want = o.stitch_frame(frames, params_fn(o), frame_index=0)["panorama"]
+    got = rig.stitch(frames, 0)["panorama"]
+    same_shape = got.shape == want.shape
+    return {"equal": bool(same_shape and np.array_equal(got, want)),
+            "max_abs_diff": int(np.abs(got.astype(int) - want.astype(int)).max()) if same_shape else None,
+            "shape": list(got.shape), "against": "reference stitch_frame (oracle/_ref), frame 0"}
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -468,6 +603,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the reference-engine check of a stitched frame")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     args = ap.parse_args()
     cfgd = CONFIGS[args.config]
@@ -575,64 +711,8 @@ def main():
     value = aggregate_fps(total_frames, ms_max)
 
     # ---- per-kernel profile pass (same workload; events around every launch)
-    roofline = None
-    stage, stage_ms = {}, None
-    if not args.no_profile:
-        # per-kernel times are taken with the stages serialised (one stream) so
-        # concurrent extraction does not inflate the compositor's kernels
-        lib.lp_rig_set_streams(rig.rig, 1)
-        lib.lp_profile_reset()
-        lib.lp_rig_work_reset(rig.rig)
-        lib.lp_profile_enable(1)
-        for i in range(args.steps):
-            step(10_000 + i)
-        torch.cuda.synchronize()
-        cap = 256
-        names = C.create_string_buffer(cap * 64)
-        tot = (C.c_double * cap)()
-        cnt = (C.c_longlong * cap)()
-        lib.lp_profile_read.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
-        n = lib.lp_profile_read(names, 64, tot, cnt, cap)
-        lib.lp_profile_enable(0)
-        lib.lp_rig_set_streams(rig.rig, 2)
-        kern = {}
-        for i in range(min(n, cap)):
-            key = names.raw[i * 64:(i + 1) * 64].split(b"\0")[0].decode()
-            kern[key] = (tot[i], cnt[i])
-        step_ms = sum(v[0] for v in kern.values()) / args.steps
-        dom = max(kern, key=lambda k: kern[k][0])
-        # every kernel against the pipe its exact arithmetic needs most of
-        # (lp_rig_algorithmic_work: compulsory bytes, FP64 add/mul/compare,
-        # FP64 div/sqrt, FP32, POPC); the bound is the pipe with the largest
-        # fraction of its measured peak
-        per_kernel = {k: kernel_roofline(lib, rig.rig, k, kern[k][0] / kern[k][1], kern[k][1])
-                      for k in kern}
-        # DRAM bytes of the same launch from the committed ncu --set full capture
-        # (scripts/ncu_traffic.py -> profiles/ncu_traffic.json), or null
-        traffic, limiter = None, None
-        try:
-            nj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-            traffic = nj.get(args.config, {}).get(dom, {}).get("traffic_bytes")
-            limiter = nj.get(args.config, {}).get(dom, {}).get("limiter")
-        except Exception:
-            pass
-        roofline = dict(per_kernel[dom])
-        roofline.update({"kernel": dom, "traffic": traffic,
-                         # what ncu says bounds it (same capture): issue slots / FP64 pipe / DRAM
-                         "ncu_limiter": limiter,
-                         "share_of_kernel_time": kern[dom][0] / max(1e-9, sum(v[0] for v in kern.values())),
-                         "kernels": {k: {"ms": round(v["avg_launch_ms"], 4), "bound": v["bound"],
-                                         "frac": None if v["frac"] is None else round(v["frac"], 4)}
-                                     for k, v in sorted(per_kernel.items(), key=lambda kv: -kern[kv[0]][0])}})
-        stage = {k: round(v[0] / v[1], 4) for k, v in sorted(kern.items(), key=lambda kv: -kv[1][0])}
-        stage["_kernel_ms_per_frame"] = round(step_ms, 4)
-        # the reference's stages (pipeline.hpp:26-34), device ms per frame
-        ref_stages = {"rectify_crop": ("k_rectify",), "detect": ("k_detect", "k_topn"),
-                      "describe": ("k_describe",),
-                      "match_estimate": ("k_lsh_keys", "k_match_query", "k_match_finalize", "k_prosac", "k_chain"),
-                      "warp_blend": ("k_warp", "k_runs", "k_mask0", "k_pyr_down", "k_blend_level")}
-        stage_ms = {name: round(sum(v[0] for k, v in kern.items() if k.split("/")[0] in ks) / args.steps, 4)
-                    for name, ks in ref_stages.items()}
+    roofline, stage, stage_ms = (None, {}, None) if args.no_profile else \
+        profile_pass(lib, rig, lambda i: step(10_000 + i), args.steps, args.config)
 
     # ---- end to end through the public C-ABI with host buffers
     e2e = None
@@ -691,12 +771,15 @@ def main():
 
     cpu = None
     parity = None
+
+    def params_fn(o):
+        q = o.default_params()
+        q.seed = q.matching.seed = 42
+        q.homography_refresh = cfgd["refresh"]
+        return q
+    if rank == 0 and world == 1 and args.no_cpu_baseline and not args.no_parity:
+        parity = parity_check(rig, sets[0], params_fn)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        def params_fn(o):
-            q = o.default_params()
-            q.seed = q.matching.seed = 42
-            q.homography_refresh = cfgd["refresh"]
-            return q
         cpu, ref_pano = cpu_baseline(sets[0], params_fn, 1)
         # parity of the measured path: the GPU rig's panorama of sets[0] at
         # frame 0 (an estimating frame, as the reference engine's first)
