@@ -76,7 +76,7 @@ def run_streams(args, cfgd, lp, world, rank, local, dist):
         rigs.append(rig)
         panos.append(torch.empty(rig.panorama_capacity(), dtype=torch.uint8, device="cuda"))
     nthreads = min(len(rigs), int(os.environ.get("LPB_CFG5_THREADS", "32")))
-    depth = int(os.environ.get("LPB_CFG5_DEPTH", "2"))
+    depth = int(os.environ.get("LPB_CFG5_DEPTH", "3"))
     groups = [list(range(i, len(rigs), nthreads)) for i in range(nthreads)]
 
     def run(steps, base, ins, outs):
@@ -130,7 +130,7 @@ def run_streams(args, cfgd, lp, world, rank, local, dist):
         fo = frame_out(panos[0].data_ptr(), fo_cap)
         roofline, stage, stage_ms = profile_pass(
             lib, rigs[0], lambda i: rigs[0].stitch_raw([x.data_ptr() for x in inputs[0]], 20_000 + i, fo),
-            args.steps, args.config)
+            max(args.steps, 50), args.config)
 
     # end to end: pinned host frames in, pinned host panoramas out
     e2e = None
