@@ -64,24 +64,47 @@ __host__ __device__ inline double geom_det(const double* h) {
     return h[0] * (h[4] * h[8] - h[5] * h[7]) - h[1] * (h[3] * h[8] - h[5] * h[6]) + h[2] * (h[3] * h[7] - h[4] * h[6]);
 }
 
-// 0 on success, else the lp_status the reference would throw
-__host__ __device__ inline int rig_geometry(int ncams, int w, int h, int blend_levels, const lp_homography* H,
-                                            RigGeom* g, double* hinv) {
+// per camera: projected-corner bbox (compute_canvas's loop body,
+// compose.hpp:44-55) and whether a corner lies behind the camera
+struct CamBox {
+    double mnx, mny, mxx, mxy;
+    int behind;
+};
+__host__ __device__ inline CamBox geom_cam_box(const double* m, int w, int h) {
+    CamBox b{1.7976931348623157e308, 1.7976931348623157e308, -1.7976931348623157e308, -1.7976931348623157e308, 0};
+    const double cs[4][2] = {{0, 0}, {static_cast<double>(w), 0}, {0, static_cast<double>(h)},
+                             {static_cast<double>(w), static_cast<double>(h)}};
+    for (int q = 0; q < 4; ++q) {
+        const double wd = m[6] * cs[q][0] + m[7] * cs[q][1] + m[8];
+        if (wd <= 0) b.behind = 1;
+        const double x = (m[0] * cs[q][0] + m[1] * cs[q][1] + m[2]) / wd;
+        const double y = (m[3] * cs[q][0] + m[4] * cs[q][1] + m[5]) / wd;
+        b.mnx = fmin(b.mnx, x);
+        b.mny = fmin(b.mny, y);
+        b.mxx = fmax(b.mxx, x);
+        b.mxy = fmax(b.mxy, y);
+    }
+    return b;
+}
+// Homography::inverse (homography.hpp:36-48), det != 0
+__host__ __device__ inline void geom_cam_inverse(const double* m, double* out) {
+    const double d = geom_det(m);
+    const double inv[9] = {(m[4] * m[8] - m[5] * m[7]) / d, (m[2] * m[7] - m[1] * m[8]) / d,
+                           (m[1] * m[5] - m[2] * m[4]) / d, (m[5] * m[6] - m[3] * m[8]) / d,
+                           (m[0] * m[8] - m[2] * m[6]) / d, (m[2] * m[3] - m[0] * m[5]) / d,
+                           (m[3] * m[7] - m[4] * m[6]) / d, (m[1] * m[6] - m[0] * m[7]) / d,
+                           (m[0] * m[4] - m[1] * m[3]) / d};
+    const double i8 = inv[8];
+    for (int j = 0; j < 9; ++j) out[j] = fabs(i8) > 1e-12 ? inv[j] / i8 : inv[j];
+}
+// canvas from the union of the boxes, then the blend levels; 0 or an lp_status
+__host__ __device__ inline int geom_canvas(const CamBox* bx, int ncams, int blend_levels, RigGeom* g) {
     double minx = 1.7976931348623157e308, miny = minx, maxx = -minx, maxy = -minx;
     for (int c = 0; c < ncams; ++c) {
-        const double* m = H[c].h;
-        if (fabs(geom_det(m)) < 1e-9) return LP_SINGULAR_HOMOGRAPHY;
-        const double cs[4][2] = {{0, 0}, {static_cast<double>(w), 0}, {0, static_cast<double>(h)},
-                                 {static_cast<double>(w), static_cast<double>(h)}};
-        for (int q = 0; q < 4; ++q) {
-            const double wd = m[6] * cs[q][0] + m[7] * cs[q][1] + m[8];
-            const double x = (m[0] * cs[q][0] + m[1] * cs[q][1] + m[2]) / wd;
-            const double y = (m[3] * cs[q][0] + m[4] * cs[q][1] + m[5]) / wd;
-            minx = fmin(minx, x);
-            miny = fmin(miny, y);
-            maxx = fmax(maxx, x);
-            maxy = fmax(maxy, y);
-        }
+        minx = fmin(minx, bx[c].mnx);
+        miny = fmin(miny, bx[c].mny);
+        maxx = fmax(maxx, bx[c].mxx);
+        maxy = fmax(maxy, bx[c].mxy);
     }
     g->ox = static_cast<int>(floor(minx));
     g->oy = static_cast<int>(floor(miny));
@@ -90,60 +113,49 @@ __host__ __device__ inline int rig_geometry(int ncams, int w, int h, int blend_l
     int levels = blend_levels;
     while (levels > 1 && (g->cw < (1 << (levels - 1)) || g->ch < (1 << (levels - 1)))) --levels;
     if (levels < 1 || levels > kMaxCompLevels) return LP_TOO_MANY_LEVELS;
-    {
-        int ww = g->cw, hh = g->ch;
-        for (int i = 1; i < levels; ++i) {
-            if (ww < 2 || hh < 2) return LP_TOO_MANY_LEVELS;
-            ww /= 2;
-            hh /= 2;
-        }
+    int ww = g->cw, hh = g->ch;
+    for (int i = 1; i < levels; ++i) {
+        if (ww < 2 || hh < 2) return LP_TOO_MANY_LEVELS;
+        ww /= 2;
+        hh /= 2;
     }
     g->levels = levels;
-    const int align = 1 << (levels - 1);
+    return 0;
+}
+// one camera's level-0 window on the canvas
+__host__ __device__ inline Win geom_cam_window(const CamBox& b, const RigGeom& g) {
+    const int align = 1 << (g.levels - 1);
     const int align_x = align > kBlendAlignX ? align : kBlendAlignX;
-    const int margin = 4 * (1 << levels) + 8;
+    const int margin = 4 * (1 << g.levels) + 8;
+    if (b.behind) return Win{0, 0, (g.cw + align_x - 1) / align_x * align_x, g.ch, 0};
+    long long x0 = static_cast<long long>(floor(b.mnx)) - g.ox - margin;
+    long long y0 = static_cast<long long>(floor(b.mny)) - g.oy - margin;
+    long long x1 = static_cast<long long>(ceil(b.mxx)) - g.ox + margin;
+    long long y1 = static_cast<long long>(ceil(b.mxy)) - g.oy + margin;
+    x0 = x0 > 0 ? (x0 / align_x) * align_x : 0;
+    y0 = y0 > 0 ? (y0 / align) * align : 0;
+    const long long xcap = (g.cw + align_x - 1) / align_x * align_x;
+    const long long xr = (x1 + align_x - 1) / align_x * align_x;
+    x1 = xr < xcap ? xr : xcap;
+    y1 = y1 < g.ch ? y1 : g.ch;
+    return Win{static_cast<int>(x0), static_cast<int>(y0), static_cast<int>(x1 - x0 > 0 ? x1 - x0 : 0),
+               static_cast<int>(y1 - y0 > 0 ? y1 - y0 : 0), 0};
+}
+
+// 0 on success, else the lp_status the reference would throw (host order:
+// a singular camera first, then the levels check)
+__host__ __device__ inline int rig_geometry(int ncams, int w, int h, int blend_levels, const lp_homography* H,
+                                            RigGeom* g, double* hinv) {
+    CamBox bx[kMaxCompCams];
     for (int c = 0; c < ncams; ++c) {
-        const double* m = H[c].h;
-        const double d = geom_det(m);
-        double inv[9] = {(m[4] * m[8] - m[5] * m[7]) / d, (m[2] * m[7] - m[1] * m[8]) / d,
-                         (m[1] * m[5] - m[2] * m[4]) / d, (m[5] * m[6] - m[3] * m[8]) / d,
-                         (m[0] * m[8] - m[2] * m[6]) / d, (m[2] * m[3] - m[0] * m[5]) / d,
-                         (m[3] * m[7] - m[4] * m[6]) / d, (m[1] * m[6] - m[0] * m[7]) / d,
-                         (m[0] * m[4] - m[1] * m[3]) / d};
-        const double i8 = inv[8];
-        for (int j = 0; j < 9; ++j) hinv[9 * c + j] = fabs(i8) > 1e-12 ? inv[j] / i8 : inv[j];
-        double mnx = 1.7976931348623157e308, mny = mnx, mxx = -mnx, mxy = -mnx;
-        bool behind = false;
-        const double cs[4][2] = {{0, 0}, {static_cast<double>(w), 0}, {0, static_cast<double>(h)},
-                                 {static_cast<double>(w), static_cast<double>(h)}};
-        for (int q = 0; q < 4; ++q) {
-            if (m[6] * cs[q][0] + m[7] * cs[q][1] + m[8] <= 0) behind = true;
-            const double wd = m[6] * cs[q][0] + m[7] * cs[q][1] + m[8];
-            const double x = (m[0] * cs[q][0] + m[1] * cs[q][1] + m[2]) / wd;
-            const double y = (m[3] * cs[q][0] + m[4] * cs[q][1] + m[5]) / wd;
-            mnx = fmin(mnx, x);
-            mny = fmin(mny, y);
-            mxx = fmax(mxx, x);
-            mxy = fmax(mxy, y);
-        }
-        Win wv{0, 0, 0, 0, 0};
-        if (behind) {
-            wv = Win{0, 0, (g->cw + align_x - 1) / align_x * align_x, g->ch, 0};
-        } else {
-            long long x0 = static_cast<long long>(floor(mnx)) - g->ox - margin;
-            long long y0 = static_cast<long long>(floor(mny)) - g->oy - margin;
-            long long x1 = static_cast<long long>(ceil(mxx)) - g->ox + margin;
-            long long y1 = static_cast<long long>(ceil(mxy)) - g->oy + margin;
-            x0 = x0 > 0 ? (x0 / align_x) * align_x : 0;
-            y0 = y0 > 0 ? (y0 / align) * align : 0;
-            const long long xcap = (g->cw + align_x - 1) / align_x * align_x;
-            const long long xr = (x1 + align_x - 1) / align_x * align_x;
-            x1 = xr < xcap ? xr : xcap;
-            y1 = y1 < g->ch ? y1 : g->ch;
-            wv = Win{static_cast<int>(x0), static_cast<int>(y0), static_cast<int>(x1 - x0 > 0 ? x1 - x0 : 0),
-                     static_cast<int>(y1 - y0 > 0 ? y1 - y0 : 0), 0};
-        }
-        g->win0[c] = wv;
+        if (fabs(geom_det(H[c].h)) < 1e-9) return LP_SINGULAR_HOMOGRAPHY;
+        bx[c] = geom_cam_box(H[c].h, w, h);
+    }
+    const int st = geom_canvas(bx, ncams, blend_levels, g);
+    if (st) return st;
+    for (int c = 0; c < ncams; ++c) {
+        geom_cam_inverse(H[c].h, hinv + 9 * c);
+        g->win0[c] = geom_cam_window(bx[c], *g);
     }
     for (int c = ncams; c < kMaxCompCams; ++c) g->win0[c] = Win{0, 0, 0, 0, 0};
     return 0;
