@@ -223,6 +223,11 @@ struct ComposeArgs {
     int Rp[kMaxCompLevels];                    // their row pitch (W[k] rounded up to 4)
     float down_taps[7];                        // gaussian_kernel(1.0f)
     DevImage src[kMaxCompCams];                // u8 grayscale cameras
+    // the same frames as 2-D textures: k_warp takes a pixel's four bilinear
+    // taps with one tex2Dgather (clamp-to-edge = the reference's x1 / y1
+    // clamp) instead of four byte loads; 0 -> byte loads
+    cudaTextureObject_t tex[kMaxCompCams];
+    int use_tex;
     int hinv_base;                             // camera c's inverse map: c_hinv[hinv_base + c]
     uint8_t* out;                              // W[0] x H[0]
     int* status;
