@@ -315,6 +315,7 @@ __global__ void __launch_bounds__(256, 4) k_detect9(const __grid_constant__ Extr
         const int cx_lo = max(rg.x0, ox - 1), cx_hi = min(rg.x1, ox + TX + 1);
 #pragma unroll 1
         for (int t0 = 0; t0 < NTASK; t0 += 256) {
+            if (t0 + (tid & ~31) >= NTASK) break;  // the tail round: warps without a task leave
             const int task = t0 + tid;
             const bool valid = task < NTASK;
             const int tk = valid ? task : 0;
@@ -422,6 +423,7 @@ __global__ void __launch_bounds__(256, 4) k_detect9(const __grid_constant__ Extr
 
     // ---- 3x3 NMS over the tile's candidates; survivors -> key list
     for (int b0 = 0; b0 < nc; b0 += 256) {
+        if (b0 + (tid & ~31) >= nc) break;  // warps past the last candidate
         const int jj = b0 + tid;
         bool keep = false;
         uint64_t key = 0;

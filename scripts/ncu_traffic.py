@@ -10,7 +10,7 @@ import json
 import os
 import sys
 
-FAMILY = {"k_detect9": "k_detect", "k_detect": "k_detect", "k_pyr_down2": "k_pyr_down", "k_describe6": "k_describe",
+FAMILY = {"k_warp_t": "k_warp", "k_detect9": "k_detect", "k_detect": "k_detect", "k_pyr_down2": "k_pyr_down", "k_describe6": "k_describe",
           "k_blend_lean": "k_blend_level", "k_blend_level": "k_blend_level",
           "k_match_query_split": "k_match_query", "k_match_query_warp": "k_match_query"}
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
