@@ -1192,6 +1192,8 @@ struct ComposeBuffers {
                 args.cov_words[c] = cdiv(w.w, 32);
                 args.cov[c] = static_cast<uint32_t*>(alloc(sizeof(uint32_t) * args.cov_words[c] * std::max(w.h, 1)));
                 args.run_rows[c] = static_cast<int2*>(alloc(sizeof(int2) * std::max(w.h, 1)));
+                args.mtile_w[c] = cdiv(w.w, kMaskTileX);
+                args.mtile[c] = static_cast<uint8_t*>(alloc(static_cast<size_t>(args.mtile_w[c]) * cdiv(std::max(w.h, 1), kMaskTileY)));
                 args.run_base[c] = static_cast<int>(total_rows * kRunSlots);
                 total_rows += w.h;
             }

@@ -16,6 +16,7 @@ struct Win {
 constexpr int kMaxCompCams = 32;   // cameras per rig on the fused compositor path
 constexpr int kMaxCompLevels = 12; // blend levels (canvas >= 2^11 px per side for 12)
 constexpr int kRunSlots = 4;       // coverage runs stored inline per window row
+constexpr int kMaskTileX = 128, kMaskTileY = 16;  // k_mask0's tile (and the mask-tile flags' grain)
 constexpr int kBlendAlignX = 64;   // level-0 window x alignment (blend tile width at level 0)
 
 // k_pyr_down output tile (level k+1) and its staged level-k box
@@ -213,6 +214,10 @@ struct ComposeArgs {
     uint32_t* cov[kMaxCompCams];               // level-0 coverage bits, cov_words per window row
     int cov_words[kMaxCompCams];
     int2* run_rows[kMaxCompCams];              // per window row: (offset into runs, count)
+    // level-0 mask tiles (k_mask0's 128 x 16 tiles of the camera window):
+    // 0 every pixel +0, 1 every pixel exactly 1, 2 mixed (null without runs)
+    uint8_t* mtile[kMaxCompCams];
+    int mtile_w[kMaxCompCams];                 // tiles per window row
     int run_base[kMaxCompCams];                // inline slots: row r of camera c owns
                                                // runs[run_base[c] + kRunSlots*r ...]
     int2* runs;                                // coverage runs [start, end) window-local
