@@ -252,7 +252,7 @@ __device__ __forceinline__ uint32_t arc9(const uint32_t (&f)[16]) {
 __global__ void __launch_bounds__(256, 4) k_detect9(const __grid_constant__ ExtractArgs a) {
     using namespace d9;
     __shared__ uint32_t s_img[SH * SWW];
-    __shared__ int s_grad[GY * GX];  // (gx & 0xffff) | gy << 16
+    __shared__ __align__(16) int s_grad[GY * GX];  // (gx & 0xffff) | gy << 16
     __shared__ float s_resp[NX * NY];
     __shared__ short s_cand[NX * NY];
     __shared__ int s_ncand, s_ninner;
@@ -296,16 +296,39 @@ __global__ void __launch_bounds__(256, 4) k_detect9(const __grid_constant__ Extr
     for (int i = tid; i < NX * NY; i += 256) s_resp[i] = __int_as_float(0x7fc00000);
     __syncthreads();
 
-    // ---- gradients (integer central differences) over the Harris support
+    // ---- gradients (integer central differences) over the Harris support,
+    // four columns per task in 16-bit lanes: gradient column gc sits at staged
+    // byte gc + xo (xo in 1..4, the same for the whole tile), so every row
+    // segment is one funnel shift of two staged words; (0x8000 + a - b) per
+    // lane cannot borrow across lanes, and its top bit flipped is (a - b)
+    // modulo 2^16: the (gx & 0xffff) | gy << 16 words come out by byte permutes
     {
-        const uint8_t* sb = reinterpret_cast<const uint8_t*>(s_img);
-        const int xo = ox - fx0;  // gradient column gc sits at staged byte gc + xo
-        for (int i = tid; i < GY * GX; i += 256) {
-            const int gr = i / GX, gc = i - gr * GX;
-            const uint8_t* p = sb + (gr + 1) * SB + gc + xo;
-            const int gx = int(p[1]) - int(p[-1]);
-            const int gy = int(p[SB]) - int(p[-SB]);
-            s_grad[i] = (gx & 0xffff) | (gy << 16);
+        const int xo = ox - fx0;
+        const int sU = 8 * (xo & 3), kU = xo >> 2;                  // bytes gc+xo .. +3 (rows above / below)
+        const int sL = 8 * ((xo - 1) & 3), kL = (xo - 1) >> 2;      // bytes gc+xo-1 .. +2 (centre row)
+        const int sR = 8 * ((xo + 1) & 3), kR = (xo + 1) >> 2;      // bytes gc+xo+1 .. +4 (centre row)
+        constexpr int GW = GX / 4;                                  // four-column groups per row
+        for (int i = tid; i < GY * GW; i += 256) {
+            const int gr = i / GW, g4 = i - gr * GW;
+            const uint32_t* row = s_img + (gr + 1) * SWW + g4;
+            const uint32_t up = __funnelshift_r(row[kU - SWW], row[kU + 1 - SWW], sU);
+            const uint32_t dn = __funnelshift_r(row[kU + SWW], row[kU + 1 + SWW], sU);
+            const uint32_t lf = __funnelshift_r(row[kL], row[kL + 1], sL);
+            const uint32_t rt = __funnelshift_r(row[kR], row[kR + 1], sR);
+            uint4 out;
+            {
+                const uint32_t dx = (__byte_perm(rt, 0, 0x4140) + 0x80008000u - __byte_perm(lf, 0, 0x4140)) ^ 0x80008000u;
+                const uint32_t dy = (__byte_perm(dn, 0, 0x4140) + 0x80008000u - __byte_perm(up, 0, 0x4140)) ^ 0x80008000u;
+                out.x = __byte_perm(dx, dy, 0x5410);
+                out.y = __byte_perm(dx, dy, 0x7632);
+            }
+            {
+                const uint32_t dx = (__byte_perm(rt, 0, 0x4342) + 0x80008000u - __byte_perm(lf, 0, 0x4342)) ^ 0x80008000u;
+                const uint32_t dy = (__byte_perm(dn, 0, 0x4342) + 0x80008000u - __byte_perm(up, 0, 0x4342)) ^ 0x80008000u;
+                out.z = __byte_perm(dx, dy, 0x5410);
+                out.w = __byte_perm(dx, dy, 0x7632);
+            }
+            *reinterpret_cast<uint4*>(&s_grad[gr * GX + 4 * g4]) = out;
         }
     }
 
