@@ -176,6 +176,15 @@ lp_status lp_extract_features(lp_ctx* ctx, const uint8_t* img, int w, int h, int
 
 /* ---- matching (matchlsh.hpp) ---- */
 
+/* query (matchlsh.hpp:132-159) of nq descriptors against the LSH index of
+ * the nt train descriptors (build_index with cfg's tables / bits / seed, the
+ * cfg.t_probes probe set, cfg.max_distance): for query q every hit within
+ * max_distance, sorted by (distance, train id), in out[offsets[q] ..
+ * offsets[q + 1]) with query_id = query_id0 + q. offsets has nq + 1 entries;
+ * *total is the hit count (out holds min(total, cap)). */
+lp_status lp_lsh_query(lp_ctx* ctx, const uint64_t* train, int nt, const uint64_t* queries, int nq, int n_d,
+                       const lp_match_config* cfg, int query_id0, long long* offsets, lp_match* out, long long cap,
+                       long long* total);
 /* descriptor_distance, matchlsh.hpp:25-33, elementwise over n pairs. */
 lp_status lp_descriptor_distances(lp_ctx* ctx, const uint64_t* a, const uint64_t* b, int n,
                                   int n_d, int* out);

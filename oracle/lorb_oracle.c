@@ -676,6 +676,75 @@ int orc_match_features(const uint64_t* a, int na, const uint64_t* b, int nb, int
     return LP_OK;
 }
 
+/* query, matchlsh.hpp:132-159, for nq queries against build_index(train):
+ * per query every probed candidate within max_distance, sorted by
+ * (distance, train_id); offsets[q] .. offsets[q + 1] index `out`. */
+int orc_lsh_query(const uint64_t* train, int nt, const uint64_t* queries, int nq, int n_d,
+                  const lp_match_config* cfg, int query_id0, long long* offsets, lp_match* out, long long cap,
+                  long long* total) {
+    *total = 0;
+    if (nq <= 0) return LP_OK;
+    for (int q = 0; q <= nq; ++q) offsets[q] = 0;
+    if (nt == 0) return LP_OK;
+    const int L = cfg->tables, k = cfg->bits, W = (n_d + 63) / 64;
+    int* pos = xcalloc((size_t)(L > 0 ? L : 1) * (k > 0 ? k : 1), sizeof(int));
+    int st = orc_lsh_bit_positions(n_d, L, k, cfg->seed, pos);
+    if (st) { free(pos); return st; }
+    uint64_t* probes = xcalloc((size_t)(cfg->t_probes > 0 ? cfg->t_probes : 1), sizeof(uint64_t));
+    st = orc_probe_sequence(k, cfg->t_probes, probes);
+    if (st) { free(pos); free(probes); return st; }
+    const int T = cfg->t_probes;
+    kid_t* tab = xcalloc((size_t)L * nt, sizeof(kid_t));
+    for (int t = 0; t < L; ++t) {
+        for (int j = 0; j < nt; ++j) {
+            tab[(size_t)t * nt + j].key = hash_key(train + (size_t)j * 2 * W, n_d, W, pos + t * k, k);
+            tab[(size_t)t * nt + j].id = j;
+        }
+        qsort(tab + (size_t)t * nt, (size_t)nt, sizeof(kid_t), kid_cmp);
+    }
+    uint8_t* seen = xcalloc((size_t)nt, 1);
+    lp_match* hits = xcalloc((size_t)nt, sizeof(lp_match));
+    long long n = 0;
+    for (int q = 0; q < nq; ++q) {
+        const uint64_t* qd = queries + (size_t)q * 2 * W;
+        memset(seen, 0, (size_t)nt);
+        int nh = 0;
+        for (int t = 0; t < L; ++t) {
+            const uint64_t key = hash_key(qd, n_d, W, pos + t * k, k);
+            const kid_t* tb = tab + (size_t)t * nt;
+            for (int p = 0; p < T; ++p) {
+                const uint64_t want = key ^ probes[p];
+                int lo = 0, hi = nt;
+                while (lo < hi) {
+                    int mid = (lo + hi) / 2;
+                    if (tb[mid].key < want) lo = mid + 1; else hi = mid;
+                }
+                for (int i = lo; i < nt && tb[i].key == want; ++i) {
+                    const int id = tb[i].id;
+                    if (seen[id]) continue;
+                    seen[id] = 1;
+                    int d = dist_packed(qd, train + (size_t)id * 2 * W, W);
+                    if (d <= cfg->max_distance) {
+                        lp_match m = {query_id0 + q, id, d, 1.0f - (float)d / (2.0f * n_d)};
+                        hits[nh++] = m;
+                    }
+                }
+            }
+        }
+        qsort(hits, (size_t)nh, sizeof(lp_match), hit_cmp);
+        for (int i = 0; i < nh; ++i, ++n)
+            if (n < cap) out[n] = hits[i];
+        offsets[q + 1] = n;
+    }
+    *total = n;
+    free(pos);
+    free(probes);
+    free(tab);
+    free(seen);
+    free(hits);
+    return LP_OK;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Homography helpers, homography.hpp:25-62 */
 static double h_det(const double* h) {

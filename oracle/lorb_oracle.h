@@ -33,6 +33,9 @@ int orc_lsh_bit_positions(int n_d, int tables, int bits, uint64_t seed, int* out
 int orc_probe_sequence(int k, int t, uint64_t* out);
 int orc_match_features(const uint64_t* a, int na, const uint64_t* b, int nb, int n_d,
                        const lp_match_config* cfg, lp_match* out, int cap, int* count);
+int orc_lsh_query(const uint64_t* train, int nt, const uint64_t* queries, int nq, int n_d,
+                  const lp_match_config* cfg, int query_id0, long long* offsets, lp_match* out, long long cap,
+                  long long* total);
 int orc_dlt_homography(const lp_corr* c, int n, lp_homography* out);
 int orc_symmetric_transfer_errors(const lp_homography* h, const lp_homography* hi, const lp_corr* c, int n,
                                   double* out);

@@ -344,20 +344,6 @@ int ref_probe_sequence(int k, int t, std::uint64_t* out) {
         std::memcpy(out, p.data(), p.size() * sizeof(std::uint64_t));
     });
 }
-int ref_lsh_query(const std::uint64_t* train, int nt, int n_d, int tables, int bits,
-                  std::uint64_t seed, const std::uint64_t* q, int t_probes, int max_distance,
-                  lp_match* out, int cap, int* count) {
-    return guard([&] {
-        std::vector<Descriptor> ds;
-        const int W2 = 2 * words(n_d);
-        for (int i = 0; i < nt; ++i) ds.push_back(unpack_desc(train + static_cast<std::size_t>(i) * W2, n_d));
-        LshIndex idx(ds, tables, bits, seed);
-        auto hits = query(idx, unpack_desc(q, n_d), t_probes, max_distance);
-        *count = static_cast<int>(hits.size());
-        for (int i = 0; i < *count && i < cap; ++i)
-            out[i] = lp_match{hits[i].query_id, hits[i].train_id, hits[i].distance, hits[i].quality};
-    });
-}
 int ref_match_features(const std::uint64_t* a, int na, const std::uint64_t* b, int nb, int n_d,
                        const lp_match_config* cfg, lp_match* out, int cap, int* count) {
     return guard([&] {
@@ -369,6 +355,32 @@ int ref_match_features(const std::uint64_t* a, int na, const std::uint64_t* b, i
         *count = static_cast<int>(m.size());
         for (int i = 0; i < *count && i < cap; ++i)
             out[i] = lp_match{m[i].query_id, m[i].train_id, m[i].distance, m[i].quality};
+    });
+}
+
+int ref_lsh_query(const std::uint64_t* train, int nt, const std::uint64_t* queries, int nq, int n_d,
+                  const lp_match_config* cfg, int query_id0, long long* offsets, lp_match* out, long long cap,
+                  long long* total) {
+    return guard([&] {
+        *total = 0;
+        if (nq <= 0) return;
+        const int W2 = 2 * words(n_d);
+        std::vector<Descriptor> st;
+        for (int i = 0; i < nt; ++i) st.push_back(unpack_desc(train + static_cast<std::size_t>(i) * W2, n_d));
+        const MatchConfig mc = match_cfg(cfg);
+        LshIndex index = build_index(st, mc.tables, mc.bits, mc.seed);
+        long long n = 0;
+        offsets[0] = 0;
+        for (int q = 0; q < nq; ++q) {
+            auto hits = query(index, unpack_desc(queries + static_cast<std::size_t>(q) * W2, n_d), mc.t_probes,
+                              mc.max_distance, query_id0 + q);
+            for (const auto& m : hits) {
+                if (n < cap) out[n] = lp_match{m.query_id, m.train_id, m.distance, m.quality};
+                ++n;
+            }
+            offsets[q + 1] = n;
+        }
+        *total = n;
     });
 }
 

@@ -131,6 +131,8 @@ _PROTOS = {
     "build_laplacian": [P, C.c_int, C.c_int, C.c_int, C.c_int, P],
     "collapse_laplacian": [P, C.c_int, C.c_int, C.c_int, C.c_int, P],
     "multiband_blend": [P, P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P],
+    "lsh_query": [P, C.c_int, P, C.c_int, C.c_int, C.POINTER(MatchConfig), C.c_int, P, P, C.c_longlong,
+                  C.POINTER(C.c_longlong)],
 }
 
 # oracle-only helpers (ref_ and orc_)
@@ -153,8 +155,6 @@ _ORACLE_EXTRA = {
 _REF_ONLY = {
     "stitch_frame_layout": [C.c_int, C.c_int, C.c_int, P, C.POINTER(Params), P, C.c_uint64,
                             C.POINTER(FrameOut)],
-    "lsh_query": [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, P, C.c_int, C.c_int, P,
-                  C.c_int, c_intp],
     "run_engine": [C.c_int, C.c_int, C.c_int, C.POINTER(Params), P, C.c_int, C.c_int, C.c_int,
                    C.c_int, c_dp, c_dp],
     "run_engines_parallel": [C.c_int, C.c_int, C.c_int, C.POINTER(Params), P, C.c_int, C.c_int,

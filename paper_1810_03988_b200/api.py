@@ -198,6 +198,23 @@ class AbiWrapper:
                    _ptr(out), cap, C.byref(n))
         return out[:n.value].copy()
 
+    def lsh_query(self, train, queries, n_d, cfg, query_id0=0):
+        """query (matchlsh.hpp:132-159) of every query against build_index(train):
+        (offsets (nq + 1), hits (total, 4) as lp_match rows)."""
+        train = np.ascontiguousarray(train, np.uint64)
+        queries = np.ascontiguousarray(queries, np.uint64)
+        nq = len(queries)
+        offsets = np.zeros(nq + 1, np.int64)
+        total = C.c_longlong()
+        cap = max(1, nq * 8)
+        while True:
+            out = np.zeros((cap, 4), np.int32)
+            self._call("lsh_query", _ptr(train), len(train), _ptr(queries), nq, n_d, C.byref(cfg), query_id0,
+                       _ptr(offsets), _ptr(out), C.c_longlong(cap), C.byref(total))
+            if total.value <= cap:
+                return offsets, out[:total.value].copy()
+            cap = total.value
+
     # ---- homography ----
     @staticmethod
     def corr_array(src, dst, quality):

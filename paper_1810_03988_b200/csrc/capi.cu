@@ -869,6 +869,47 @@ lp_status lp_match_features(lp_ctx* ctx, const uint64_t* set_a, int na, const ui
     });
 }
 
+lp_status lp_lsh_query(lp_ctx* ctx, const uint64_t* train, int nt, const uint64_t* queries, int nq, int n_d,
+                       const lp_match_config* cfg, int query_id0, long long* offsets, lp_match* out, long long cap,
+                       long long* total) {
+    return guard([&] {
+        *total = 0;
+        if (nq <= 0) return;
+        if (nt == 0) {
+            for (int q = 0; q <= nq; ++q) offsets[q] = 0;
+            return;
+        }
+        cudaStream_t s = ctx->stream;
+        MatchTables T(n_d, *cfg, s);
+        const int W2 = 2 * ((n_d + 63) / 64);
+        const int capn = std::max(nq, nt);
+        DBuf desc(sizeof(uint64_t) * 2 * capn * W2, s), counts(sizeof(int) * 2, s),
+            keys(sizeof(uint64_t) * 2 * capn * std::max(cfg->tables, 1), s);
+        auto kind = [](const void* p) { return is_device_ptr(p) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice; };
+        LPB_CUDA(cudaMemcpyAsync(desc.p, train, sizeof(uint64_t) * nt * W2, kind(train), s));
+        LPB_CUDA(cudaMemcpyAsync(desc.as<uint64_t>() + static_cast<size_t>(capn) * W2, queries,
+                                 sizeof(uint64_t) * nq * W2, kind(queries), s));
+        int hc[2] = {nt, nq};
+        LPB_CUDA(cudaMemcpyAsync(counts.p, hc, sizeof hc, cudaMemcpyHostToDevice, s));
+        MatchArgs a{};
+        a.npairs = 1;
+        a.qslot0 = 1;
+        a.tslot0 = 0;
+        a.nslots = 2;
+        a.desc = desc.as<uint64_t>();
+        a.counts = counts.as<int>();
+        a.cap = capn;
+        a.n_d = n_d;
+        T.fill(a, *cfg);
+        a.keys = keys.as<uint64_t>();
+        Out<lp_match> dout(out, static_cast<size_t>(std::max<long long>(cap, 0)), s);
+        const long long n = lsh_query_launch(a, nq, query_id0, offsets, dout.d, cap, s);
+        dout.finish(s, static_cast<size_t>(std::min(n, cap)));
+        LPB_CUDA(cudaStreamSynchronize(s));
+        *total = n;
+    });
+}
+
 // ---------------------------------------------------------------------------
 lp_status lp_dlt_homography(lp_ctx* ctx, const lp_corr* pairs, int n, lp_homography* out) {
     return guard([&] {

@@ -14,6 +14,9 @@
 #include "match.cuh"
 #include "prims.cuh"
 
+#include <algorithm>
+#include <vector>
+
 namespace lpb {
 
 // one warp per descriptor: lane b extracts bit b of a table's key (hash_key,
@@ -310,6 +313,104 @@ __global__ void k_match_emit(MatchArgs a, int pair, const uint32_t* keys) {
     a.corr[static_cast<size_t>(pair) * a.cap + i] = c;
 }
 __global__ void k_zero_int(int* p) { *p = 0; }
+
+// ---- query(): every candidate within max_distance, one warp per query.
+// Pass 1 counts each query's hits, pass 2 writes (query, distance, id) as a
+// 64-bit key (query << 43 | distance << 32 | id) into the query's segment;
+// one stable radix sort of the keys orders every segment by (distance, id).
+template <bool EMIT>
+__global__ void __launch_bounds__(256) k_lsh_query(MatchArgs a, int nq, unsigned* count, const unsigned* offset,
+                                                   uint32_t* key_lo, uint32_t* key_hi) {
+    const int q = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (q >= nq) return;
+    const int qs = a.qslot0, ts = a.tslot0;
+    const int nt = a.counts[ts];
+    const int W = (a.n_d + 63) / 64;
+    const uint64_t* tkeys = a.keys + static_cast<size_t>(ts) * a.cap * a.tables;
+    const uint64_t* qkeys = a.keys + (static_cast<size_t>(qs) * a.cap + q) * a.tables;
+    const uint64_t* qd = a.desc + (static_cast<size_t>(qs) * a.cap + q) * 2 * W;
+    const uint64_t* tdesc = a.desc + static_cast<size_t>(ts) * a.cap * 2 * W;
+    unsigned pos = EMIT ? offset[q] : 0u, n = 0;
+    for (int j0 = 0; j0 < nt; j0 += 32) {
+        const int j = j0 + lane;
+        bool hit = false;
+        int d = 0;
+        if (j < nt) {
+            bool cand = false;
+            for (int t = 0; t < a.tables && !cand; ++t)
+                cand = in_probe_set(qkeys[t] ^ tkeys[static_cast<size_t>(j) * a.tables + t], a);
+            if (cand) {
+                const uint64_t* td = tdesc + static_cast<size_t>(j) * 2 * W;
+                for (int w = 0; w < 2 * W; ++w) d += __popcll(qd[w] ^ td[w]);
+                hit = d <= a.max_distance;
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (EMIT && hit) {
+            const unsigned slot = pos + n + __popc(m & ((1u << lane) - 1u));
+            key_lo[slot] = static_cast<uint32_t>(j);
+            key_hi[slot] = (static_cast<uint32_t>(q) << 11) | static_cast<uint32_t>(d);
+        }
+        n += __popc(m);
+    }
+    if (!EMIT && lane == 0) count[q] = n;
+}
+__global__ void k_lsh_query_out(MatchArgs a, long long total, long long cap, int query_id0, const uint32_t* key_lo,
+                                const uint32_t* key_hi, const int* order, lp_match* out) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= total || i >= cap) return;
+    const int s = order[i];
+    lp_match m;
+    m.query_id = query_id0 + static_cast<int>(key_hi[s] >> 11);
+    m.train_id = static_cast<int>(key_lo[s]);
+    m.distance = static_cast<int>(key_hi[s] & 0x7FFu);
+    m.quality = fsub(1.0f, __fdiv_rn(static_cast<float>(m.distance), fmul(2.0f, static_cast<float>(a.n_d))));
+    out[i] = m;
+}
+__global__ void k_gather_u32(const uint32_t* src, const int* idx, long long n, uint32_t* dst) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[idx[i]];
+}
+__global__ void k_iota_q(int* p, long long n) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = static_cast<int>(i);
+}
+
+long long lsh_query_launch(const MatchArgs& a, int nq, int query_id0, long long* offsets, lp_match* out,
+                           long long cap, cudaStream_t s) {
+    if (nq <= 0) return 0;
+    if (a.n_d > 64 * kMaxW) throw Status(LP_BAD_PARAMS, "query: n_d too large");
+    if (nq >= (1 << 21)) throw Status(LP_BAD_PARAMS, "query: too many queries in one call");
+    if (!a.keys_ready)
+        LPB_LAUNCH(k_lsh_keys, cdiv(static_cast<long long>(a.nslots) * a.cap * 32, 256), 256, 0, s, a);
+    DBuf cnt(sizeof(unsigned) * (nq + 1), s), tot(sizeof(int), s);
+    LPB_LAUNCH(k_lsh_query<false>, cdiv(nq, 8), 256, 0, s, a, nq, cnt.as<unsigned>(),
+               static_cast<const unsigned*>(nullptr), static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr));
+    LPB_LAUNCH(k_scan_exclusive, 1, 1024, 0, s, cnt.as<unsigned>(), nq + 1, tot.as<int>());
+    std::vector<unsigned> off(nq + 1);
+    LPB_CUDA(cudaMemcpyAsync(off.data(), cnt.p, sizeof(unsigned) * (nq + 1), cudaMemcpyDeviceToHost, s));
+    LPB_CUDA(cudaStreamSynchronize(s));
+    const long long total = off[nq];
+    for (int q = 0; q <= nq; ++q) offsets[q] = off[q];
+    if (total == 0) return 0;
+    if (total >= (1LL << 31)) throw Status(LP_CAPACITY_OVERFLOW, "query: too many hits");
+    const int n = static_cast<int>(total);
+    DBuf lo(sizeof(uint32_t) * n, s), hi(sizeof(uint32_t) * n, s), ka(sizeof(uint32_t) * n, s),
+        kb(sizeof(uint32_t) * n, s), ia(sizeof(int) * n, s), ib(sizeof(int) * n, s),
+        hist(sizeof(unsigned) * 256 * cdiv(n, kPrimTile), s);
+    LPB_LAUNCH(k_lsh_query<true>, cdiv(nq, 8), 256, 0, s, a, nq, static_cast<unsigned*>(nullptr), cnt.as<unsigned>(),
+               lo.as<uint32_t>(), hi.as<uint32_t>());
+    // (query, distance) major, train id minor: stable by id, then by the high word
+    LPB_LAUNCH(k_iota_q, cdiv(n, 256), 256, 0, s, ia.as<int>(), static_cast<long long>(n));
+    LPB_CUDA(cudaMemcpyAsync(ka.p, lo.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s));
+    radix_sort_pairs(ka.as<uint32_t>(), ia.as<int>(), kb.as<uint32_t>(), ib.as<int>(), n, 32, hist.as<unsigned>(), s);
+    LPB_LAUNCH(k_gather_u32, cdiv(n, 256), 256, 0, s, hi.as<uint32_t>(), ia.as<int>(), static_cast<long long>(n),
+               ka.as<uint32_t>());
+    radix_sort_pairs(ka.as<uint32_t>(), ia.as<int>(), kb.as<uint32_t>(), ib.as<int>(), n, 32, hist.as<unsigned>(), s);
+    LPB_LAUNCH(k_lsh_query_out, cdiv(std::min<long long>(n, cap), 256), 256, 0, s, a, total, cap, query_id0,
+               lo.as<uint32_t>(), hi.as<uint32_t>(), ia.as<int>(), out);
+    return total;
+}
 
 void match_launch(const MatchArgs& a, cudaStream_t s) {
     if (a.npairs <= 0) return;

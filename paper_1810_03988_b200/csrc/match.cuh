@@ -30,4 +30,12 @@ struct MatchArgs {
 
 void match_launch(const MatchArgs& a, cudaStream_t s);
 
+// query (matchlsh.hpp:132-159) for nq query descriptors (slot qslot0) against
+// the index of slot tslot0: every train descriptor reached by a probed bucket
+// of some table, within max_distance, sorted by (distance, id). Output:
+// offsets[q] .. offsets[q + 1] index `out` (query_id = query_id0 + q).
+// Returns the total hit count (host sync); out holds min(total, cap) hits.
+long long lsh_query_launch(const MatchArgs& a, int nq, int query_id0, long long* offsets, lp_match* out,
+                           long long cap, cudaStream_t s);
+
 }  // namespace lpb
