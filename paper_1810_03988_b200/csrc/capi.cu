@@ -1176,7 +1176,7 @@ struct ComposeBuffers {
     std::vector<std::unique_ptr<DBuf>> bufs;
     ComposeArgs args{};
 
-    DBuf runs, runs_used, status;
+    DBuf runs, runs_used, status, mask_state;
     std::vector<float*> host_G, host_M;  // [c * levels + k]
     std::vector<PyrTma> pyr_tma;         // per source level k: k_pyr_down2's tensor maps
     std::vector<BlendTma> blend_tma;     // per level k < levels - 1: k_blend_lean's tensor maps
@@ -1250,12 +1250,23 @@ struct ComposeBuffers {
             runs_used = DBuf(sizeof(int), s);
             args.runs = runs.as<int2>();
             args.runs_used = runs_used.as<int>();
+            // masks of fresh arenas are never current (LPB_MASK_REUSE=0: recompute every frame)
+            const char* e = std::getenv("LPB_MASK_REUSE");
+            if (!(e && e[0] == '0')) {
+                mask_state = DBuf(sizeof(MaskState), s);
+                LPB_CUDA(cudaMemsetAsync(mask_state.p, 0, sizeof(MaskState), s));
+                args.mask_state = mask_state.as<MaskState>();
+            }
         }
         status = DBuf(sizeof(int), s);
         LPB_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int), s));
         args.status = status.as<int>();
         auto taps = host::gaussian_kernel(1.0f);
         for (int q = 0; q < 7; ++q) args.down_taps[q] = taps[q];
+        {   // level-0 blend tiles covered by one camera at weight 1 (LPB_BLEND_UNIT=0: off)
+            const char* e = std::getenv("LPB_BLEND_UNIT");
+            args.blend_unit = (e && e[0] == '0') ? 0 : 1;
+        }
         // TMA staging of the pyramid boxes (LPB_TMA=0: cp.async everywhere)
         pyr_tma.assign(std::max(levels - 1, 1), PyrTma{});
         args.pyr_tma = nullptr;

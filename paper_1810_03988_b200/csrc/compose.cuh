@@ -203,6 +203,13 @@ struct GeomArgs {
 void geom_launch(const GeomArgs& a, cudaStream_t s);
 
 // Passed by value (constant bank): all per-camera geometry and pointers.
+struct MaskState {
+    int valid;  // this frame's maps equal `key`: every mask buffer is current
+    int have;   // `key` holds the maps of the last compose that made the masks
+    unsigned next_runs, next_mask0;  // k_runs / k_mask0 work counters (reset by k_warp)
+    double key[kMaxCompCams][9];
+};
+
 struct ComposeArgs {
     int ncams, levels;
     int W[kMaxCompLevels], H[kMaxCompLevels];  // canvas dims per level
@@ -233,6 +240,13 @@ struct ComposeArgs {
     // clamp) instead of four byte loads; 0 -> byte loads
     cudaTextureObject_t tex[kMaxCompCams];
     int use_tex;
+    int blend_unit;                            // k_blend_lean's single-camera unit-weight tiles
+    // seam masks (coverage runs, M pyramid, tile flags) depend only on the
+    // inverse maps and the windows: k_warp's first CTA compares this frame's
+    // maps with the ones the arenas' masks were made from and sets `valid`;
+    // k_runs / k_mask0 / the mask half of k_pyr_down then skip. Null: always
+    // recompute (caller-provided masks, LPB_MASK_REUSE=0)
+    struct MaskState* mask_state;
     int hinv_base;                             // camera c's inverse map: c_hinv[hinv_base + c]
     uint8_t* out;                              // W[0] x H[0]
     int* status;

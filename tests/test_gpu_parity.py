@@ -544,6 +544,46 @@ def test_async_reregistration_geometry_changes(lp, orc, in_flight):
         assert np.array_equal(g["panorama"], want["panorama"]), t
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("in_flight", [1, 3])
+def test_mask_reuse_across_cached_frames(lp, orc, in_flight):
+    """Seam masks, coverage runs and the mask pyramid depend only on the
+    inverse maps and windows, so frames composed on the maps of the previous
+    frame reuse them (MaskState) while their image pyramids are rebuilt from
+    new content. Frames here change content every frame and re-register
+    every third (new maps, same or moved geometry): every panorama equals the
+    oracle's for that frame."""
+    from paper_1810_03988_b200 import Rig
+    p = orc.default_params()
+    p.seed = p.matching.seed = 42
+    p.homography_refresh = 3
+    frames = [orc.planted_pair(480, 270, 0.25 + 0.05 * (t // 3 % 2), 11 + t)[:2] for t in range(8)]
+    rig = Rig(lp, 2, 480, 270, p)
+    got, inflight = {}, []
+    for t, (l, r) in enumerate(frames):
+        inflight.append((t, rig.submit_frame([l, r], t)))
+        if len(inflight) >= in_flight:
+            t0, hnd = inflight.pop(0)
+            got[t0] = rig.wait_frame(hnd)
+    for t0, hnd in inflight:
+        got[t0] = rig.wait_frame(hnd)
+    homs = None
+    for t, (l, r) in enumerate(frames):
+        if t % 3 == 0:  # re-registration: the whole frame from a fresh oracle engine
+            want = orc.stitch_frame([l, r], p, frame_index=t)
+            homs, canvas, pano = want["homographies"], want["canvas"], want["panorama"]
+        else:  # the cached set: warp_blend (pipeline.hpp:499-521) with the oracle's primitives
+            canvas, _ = orc.compute_canvas([(480, 270)] * 2, homs)
+            warped = [orc.warp_image(img.astype(np.float32), homs[c], canvas) for c, img in enumerate((l, r))]
+            masks = orc.linear_seam_mask(np.stack([cv for _, cv in warped]))
+            pano = orc.multiband_blend(np.stack([wi for wi, _ in warped]), masks, p.blend_levels)
+        g = got[t]
+        assert g["canvas"] == canvas, (t, g["canvas"], canvas)
+        assert np.array_equal(g["homographies"], homs), t
+        assert np.array_equal(g["panorama"], pano), t
+
+
+@pytest.mark.gpu
 def test_concurrent_rigs_threads(lp, orc):
     """Independent rigs on one context, driven from host threads (the config-5
     shape): each rig has its own stage stream, so their frames overlap on the
