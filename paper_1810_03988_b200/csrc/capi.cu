@@ -12,6 +12,8 @@
 
 #include <atomic>
 #include <cctype>
+#include <chrono>
+#include <cstdio>
 #include <deque>
 #include <fstream>
 #include <map>

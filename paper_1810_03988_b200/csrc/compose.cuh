@@ -162,12 +162,21 @@ __host__ __device__ inline int rig_geometry(int ncams, int w, int h, int blend_l
     return 0;
 }
 
-__host__ __device__ inline bool same_geometry(const RigGeom& a, const RigGeom& b, int ncams) {
-    if (a.cw != b.cw || a.ch != b.ch || a.ox != b.ox || a.oy != b.oy || a.levels != b.levels) return false;
-    for (int c = 0; c < ncams; ++c)
-        if (a.win0[c].x0 != b.win0[c].x0 || a.win0[c].y0 != b.win0[c].y0 || a.win0[c].w != b.win0[c].w ||
-            a.win0[c].h != b.win0[c].h)
+
+// Can arenas built for `ref` compose a frame of geometry `g`? The same canvas
+// and levels, and every camera's window inside ref's: a larger window only
+// computes more of the reference's zero canvas around the camera (DESIGN.md
+// §3, windows), and ref's windows keep the alignment the blend tiles need.
+// Small homography jitter between re-registrations then keeps the arenas.
+__host__ __device__ inline bool fits_geometry(const RigGeom& g, const RigGeom& ref, int ncams) {
+    if (g.cw != ref.cw || g.ch != ref.ch || g.ox != ref.ox || g.oy != ref.oy || g.levels != ref.levels) return false;
+    for (int c = 0; c < ncams; ++c) {
+        const Win& a = g.win0[c];
+        const Win& b = ref.win0[c];
+        if (a.w == 0 || a.h == 0) continue;
+        if (b.w == 0 || b.h == 0 || a.x0 < b.x0 || a.y0 < b.y0 || a.x0 + a.w > b.x0 + b.w || a.y0 + a.h > b.y0 + b.h)
             return false;
+    }
     return true;
 }
 

@@ -41,6 +41,7 @@
 #include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <deque>
 #include <functional>
@@ -408,6 +409,15 @@ public:
         else
             run_pipelined(source, sink, m);
         m.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
+        if (std::getenv("LPB_ENGINE_PROFILE"))  // host time per frame in the engine's own steps
+            std::fprintf(stderr, "engine host ms/frame: launch %.4f (regions %.4f staging %.4f submit %.4f) wait %.4f fill %.4f over %llu frames\n",
+                         prof_[0] / 1e6 / std::max<std::uint64_t>(m.frames_out, 1),
+                         prof_[4] / 1e6 / std::max<std::uint64_t>(m.frames_out, 1),
+                         prof_[5] / 1e6 / std::max<std::uint64_t>(m.frames_out, 1),
+                         prof_[1] / 1e6 / std::max<std::uint64_t>(m.frames_out, 1),
+                         prof_[2] / 1e6 / std::max<std::uint64_t>(m.frames_out, 1),
+                         prof_[3] / 1e6 / std::max<std::uint64_t>(m.frames_out, 1),
+                         static_cast<unsigned long long>(m.frames_out));
         m.frames_per_second = m.wall_seconds > 0 ? m.frames_out / m.wall_seconds : 0.0;
         if (pool_) {
             m.pool_creations = pool_->arena_creations();
@@ -854,9 +864,16 @@ private:
     }
 
     void launch(Flight& f, std::unique_ptr<FramePacket> pkt, Metrics& m) {
+        const std::int64_t t_launch = detail::now_ns();
+        struct Acc {
+            std::int64_t& s;
+            std::int64_t t0;
+            ~Acc() { s += detail::now_ns() - t0; }
+        } acc{prof_[0], t_launch};
         FramePacket& p = *pkt;
         f.pkt = std::move(pkt);
         f.ticket = 0;
+        const std::int64_t t_rect = detail::now_ns();
         const bool rectified = timed_stage(p, Stage::RectifyCrop, m, [&] {
             if (layout_is_identity()) {
                 std::vector<std::pair<int, int>> dims;
@@ -866,6 +883,7 @@ private:
                 stage_rectify_crop(p);
             }
         });
+        prof_[4] += detail::now_ns() - t_rect;
         if (!rectified) return;
         if (!rig_fits(p)) {
             run_stage_bodies(p, m);
@@ -890,6 +908,7 @@ private:
             o.cap_kp = cap_kp;
             o.matches = f.matches.get<lp_match>(np * cap_kp);
             o.cap_matches = cap_kp;
+            const std::int64_t t_stage = detail::now_ns();
             std::uint8_t* staged = f.frames.get<std::uint8_t>(ncams * fb);
             std::vector<const std::uint8_t*> ims(ncams);
             for (int c = 0; c < ncams; ++c) {
@@ -897,7 +916,9 @@ private:
                 ims[c] = staged + c * fb;
             }
             f.t_submit = detail::now_ns();
+            prof_[5] += f.t_submit - t_stage;
             const lp_status st = lp_rig_submit_frame(rig_, ims.data(), p.frame_index, &o, &f.ticket);
+            prof_[1] += detail::now_ns() - f.t_submit;
             if (st != LP_OK) {
                 note_drop(p, stage_of(st), lp_last_error(), m);
                 f.ticket = 0;
@@ -912,11 +933,15 @@ private:
     std::unique_ptr<FramePacket> land(Flight& f, Metrics& m) {
         FramePacket& p = *f.pkt;
         if (f.ticket != 0 && !p.failed) {
+            const std::int64_t t0 = detail::now_ns();
             const lp_status st = lp_rig_wait_frame(rig_, f.ticket, &f.out);
+            const std::int64_t t1 = detail::now_ns();
+            prof_[2] += t1 - t0;
             if (st != LP_OK) {
                 note_drop(p, stage_of(st), lp_last_error(), m);
             } else {
                 fill_packet(f, m);
+                prof_[3] += detail::now_ns() - t1;
             }
         }
         return std::move(f.pkt);
@@ -982,6 +1007,7 @@ private:
     int rig_cams_ = 0, rig_w_ = 0, rig_h_ = 0;
     std::array<Flight, 3> flights_;
     std::mutex metrics_mu_;
+    std::int64_t prof_[6] = {};  // host ns: launch, submit call, wait call, fill, rectify/regions, staging (LPB_ENGINE_PROFILE)
 };
 
 /// A pool sized for `frames_in_flight` packets (pipeline.hpp:724-735).

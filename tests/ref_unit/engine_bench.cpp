@@ -17,6 +17,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <algorithm>
+#include <chrono>
 
 #include "lorbpano/pipeline.hpp"
 #include "lorbpano/synth.hpp"
@@ -28,13 +30,21 @@ int main(int argc, char** argv) {
     const int frames = argc > 2 ? std::atoi(argv[2]) : 10;
     const bool piped = argc > 3 && std::string(argv[3]) == "pipelined";
     int cams = 2, w = 640, h = 480, refresh = 1;
+    // crit9: acceptance.cpp:385-416 (criterion 9's workload): 320x240 pair,
+    // overlap 0.4, top_n 200, seed 99, the default refresh interval
+    const bool crit9 = cfg == "crit9";
+    if (crit9) {
+        w = 320;
+        h = 240;
+        refresh = PipelineConfig{}.homography_refresh;
+    }
     if (cfg == "cfg3") {
         cams = 4;
         w = 3840;
         h = 2160;
         refresh = 1 << 30;
     }
-    const double overlap = 0.25;
+    const double overlap = crit9 ? 0.4 : 0.25;
     std::vector<ImageU8> chain;
     synth::PlantedPair scene;
     if (cfg == "cfg3") {
@@ -47,7 +57,7 @@ int main(int argc, char** argv) {
             chain.push_back(std::move(img));
         }
     } else {
-        scene = synth::planted_pair(w, h, overlap, 42);
+        scene = synth::planted_pair(w, h, overlap, crit9 ? 909 : 42);
     }
     RigLayout rig;
     rig.cameras.resize(cams);
@@ -55,6 +65,11 @@ int main(int argc, char** argv) {
     StitchParams params;
     params.seed = 42;
     params.matching.seed = 42;
+    if (crit9) {
+        params = StitchParams{};
+        params.extraction.top_n = 200;
+        params.seed = 99;
+    }
     PipelineConfig pc;
     pc.mode = piped ? PipelineMode::Pipelined : PipelineMode::Serial;
     pc.frames_in_flight = 4;
@@ -63,14 +78,26 @@ int main(int argc, char** argv) {
     int produced = 0;
     std::uint64_t sum = 0, fnv = 1469598103934665603ULL, first_fnv = 0;
     int outw = 0, outh = 0, delivered = 0;
+    double source_s = 0, sink_s = 0;  // time inside the callbacks
+    auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
     Metrics m = engine.run(
         [&]() -> std::optional<std::vector<ImageU8>> {
             if (produced >= frames) return std::nullopt;
             const int f = produced++;
             if (cfg == "cfg3") return chain;
-            return synth::sequence_frame(scene, static_cast<std::uint64_t>(f));
+            const double t0 = now();
+            auto fr = synth::sequence_frame(scene, static_cast<std::uint64_t>(f));
+            source_s += now() - t0;
+            return fr;
         },
         [&](const FramePacket& pkt) {
+            const double t0 = now();
+            struct Acc {
+                double& s;
+                double t0;
+                double (*clock)();
+                ~Acc() { s += clock() - t0; }
+            } acc{sink_s, t0, +[] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }};
             outw = pkt.composite.width;
             outh = pkt.composite.height;
             // the first composite fully hashed; later ones by a strided
@@ -86,7 +113,9 @@ int main(int argc, char** argv) {
             }
             if (delivered++ == 0) first_fnv = f1;
         });
-    std::printf("{\"config\": \"%s\", \"mode\": \"%s\", \"frames\": %llu, \"frames_per_second\": %.4f, "
+    std::printf("{\"source_ms\": %.4f, \"sink_ms\": %.4f, ", 1e3 * source_s / std::max(frames, 1),
+                1e3 * sink_s / std::max(frames, 1));
+    std::printf("\"config\": \"%s\", \"mode\": \"%s\", \"frames\": %llu, \"frames_per_second\": %.4f, "
                 "\"wall_seconds\": %.4f, \"drops\": %zu, \"canvas\": [%d, %d], \"composite_sum\": %llu, "
                 "\"composite_fnv\": \"%016llx\", \"first_fnv\": \"%016llx\", \"estimations\": %llu, \"stage_mean_ms\": {",
                 cfg.c_str(), piped ? "pipelined" : "serial", static_cast<unsigned long long>(m.frames_out),
