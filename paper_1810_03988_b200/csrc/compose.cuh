@@ -40,7 +40,12 @@ struct BlendTma {
     int ok;
 };
 // staged coarse tile of k_blend_lean<TXK>: rows, columns (16-byte rows)
-__host__ __device__ constexpr int lean_cy(int txk) { return 4096 / txk / 2 + 3; }
+// k_blend_lean's tile: kLeanPx pixels for kLeanThreads threads (16 per thread)
+#ifndef LPB_LEAN_PX
+#define LPB_LEAN_PX 2048
+#endif
+constexpr int kLeanPx = LPB_LEAN_PX, kLeanThreads = LPB_LEAN_PX / 16;
+__host__ __device__ constexpr int lean_cy(int txk) { return kLeanPx / txk / 2 + 3; }
 __host__ __device__ constexpr int lean_cx(int txk) { return (txk / 2 + 3 + 3 + 3) / 4 * 4; }
 
 // Encode a 2-D f32 tensor map (w x h elements, row pitch `pitch` elements,
