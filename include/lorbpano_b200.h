@@ -301,6 +301,11 @@ lp_status lp_rig_create(lp_ctx* ctx, int ncams, int w, int h, const lp_params* p
 lp_status lp_rig_create_layout(lp_ctx* ctx, int ncams, int w, int h, const lp_camera* cams,
                                const lp_params* params, lp_rig** out);
 void lp_rig_destroy(lp_rig* rig);
+/* A new StitchEngine's state on an existing rig (pipeline.hpp:343-350 with
+ * the same layout and parameters): waits for the frames in flight, then
+ * forgets the cached homographies (HomographyCache empty again) and every
+ * per-frame record; device arenas, graphs and staging are kept. */
+lp_status lp_rig_reset(lp_rig* rig);
 /* One frame through detect -> describe -> match_estimate (HomographyCache,
  * pipeline.hpp:259-286) -> warp_blend. images[c] host or device. */
 lp_status lp_rig_stitch(lp_rig* rig, const uint8_t* const* images, uint64_t frame_index,

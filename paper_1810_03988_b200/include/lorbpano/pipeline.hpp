@@ -324,6 +324,54 @@ using FrameSource = std::function<std::optional<std::vector<ImageU8>>()>;
 using FrameSink = std::function<void(const FramePacket&)>;
 
 namespace detail {
+
+// Device rigs of finished engines, kept for the next engine of the same
+// layout, frame size and parameters (a rig does not depend on the context
+// it was created through, and serves one engine at a time): creating
+// one (device arenas, pinned staging, textures, graphs) costs 5-300 ms,
+// which an engine of a few hundred small frames would otherwise spend
+// mostly there. A taken rig is reset to an empty HomographyCache
+// (lp_rig_reset), so nothing of the previous engine's state carries over.
+// Two idle rigs at most; the pool itself is never destroyed (rigs left in it
+// at process exit go with the process).
+class RigPool {
+public:
+    lp_rig* take(int ncams, int w, int h, const lp_params& p) {
+        std::lock_guard<std::mutex> l(mu_);
+        for (std::size_t i = 0; i < idle_.size(); ++i) {
+            const Entry& e = idle_[i];
+            if (e.ncams == ncams && e.w == w && e.h == h && std::memcmp(&e.p, &p, sizeof p) == 0) {
+                lp_rig* r = e.rig;
+                idle_.erase(idle_.begin() + static_cast<std::ptrdiff_t>(i));
+                if (lp_rig_reset(r) == LP_OK) return r;
+                lp_rig_destroy(r);
+                return nullptr;
+            }
+        }
+        return nullptr;
+    }
+    void give(lp_rig* r, int ncams, int w, int h, const lp_params& p) {
+        std::lock_guard<std::mutex> l(mu_);
+        if (idle_.size() >= 2) {
+            lp_rig_destroy(idle_.front().rig);
+            idle_.erase(idle_.begin());
+        }
+        idle_.push_back(Entry{r, ncams, w, h, p});
+    }
+
+private:
+    struct Entry {
+        lp_rig* rig;
+        int ncams, w, h;
+        lp_params p;
+    };
+    std::mutex mu_;
+    std::vector<Entry> idle_;
+};
+inline RigPool& rig_pool() {
+    static RigPool* pool = new RigPool;  // outlives every engine, including static ones
+    return *pool;
+}
 // A bounded FIFO between the engine's threads; close() releases the waiters.
 template <class T>
 class Channel {
@@ -410,7 +458,8 @@ public:
             run_pipelined(source, sink, m);
         m.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
         if (std::getenv("LPB_ENGINE_PROFILE"))  // host time per frame in the engine's own steps
-            std::fprintf(stderr, "engine host ms/frame: launch %.4f (regions %.4f staging %.4f submit %.4f) wait %.4f fill %.4f over %llu frames\n",
+            std::fprintf(stderr, "engine rig creation %.3f ms; host ms/frame: launch %.4f (regions %.4f staging %.4f submit %.4f) wait %.4f fill %.4f over %llu frames\n",
+                         prof_[6] / 1e6,
                          prof_[0] / 1e6 / std::max<std::uint64_t>(m.frames_out, 1),
                          prof_[4] / 1e6 / std::max<std::uint64_t>(m.frames_out, 1),
                          prof_[5] / 1e6 / std::max<std::uint64_t>(m.frames_out, 1),
@@ -748,7 +797,7 @@ private:
     }
 
     void drop_rig() {
-        if (rig_) lp_rig_destroy(rig_);
+        if (rig_) detail::rig_pool().give(rig_, rig_cams_, rig_w_, rig_h_, rig_params_);
         rig_ = nullptr;
     }
 
@@ -766,7 +815,11 @@ private:
         p.homography_refresh = cfg_.homography_refresh;
         p.seed = params_.seed;
         p.overlap_fraction = layout_.overlap.overlap_fraction;
-        b200::check(lp_rig_create(b200::ctx(), ncams, w, h, &p, &rig_));
+        const std::int64_t t0 = detail::now_ns();
+        rig_ = detail::rig_pool().take(ncams, w, h, p);
+        if (!rig_) b200::check(lp_rig_create(b200::ctx(), ncams, w, h, &p, &rig_));
+        prof_[6] += detail::now_ns() - t0;
+        rig_params_ = p;
         rig_cams_ = ncams;
         rig_w_ = w;
         rig_h_ = h;
@@ -1005,9 +1058,10 @@ private:
     bool warmup_noted_ = false;
     lp_rig* rig_ = nullptr;
     int rig_cams_ = 0, rig_w_ = 0, rig_h_ = 0;
+    lp_params rig_params_{};
     std::array<Flight, 3> flights_;
     std::mutex metrics_mu_;
-    std::int64_t prof_[6] = {};  // host ns: launch, submit call, wait call, fill, rectify/regions, staging (LPB_ENGINE_PROFILE)
+    std::int64_t prof_[7] = {};  // host ns: launch, submit call, wait call, fill, rectify/regions, staging (LPB_ENGINE_PROFILE)
 };
 
 /// A pool sized for `frames_in_flight` packets (pipeline.hpp:724-735).

@@ -95,6 +95,8 @@ def load():
         lib.lp_rig_algorithmic_work.restype = C.c_int
         lib.lp_rig_work_reset.argtypes = [P]
         lib.lp_rig_work_reset.restype = C.c_int
+        lib.lp_rig_reset.argtypes = [P]
+        lib.lp_rig_reset.restype = C.c_int
         lib.lp_profile_enable.argtypes = [C.c_int]
         lib.lp_profile_enable.restype = None
         lib.lp_profile_reset.argtypes = []
@@ -189,6 +191,10 @@ class Rig:
             _check(self.lib, self.lib.lp_rig_create_layout(lorb.ctx, ncams, w, h, cams, C.byref(params),
                                                            C.byref(r)))
         self.rig = r
+
+    def reset(self):
+        """A fresh HomographyCache on this rig's device resources (lp_rig_reset)."""
+        _check(self.lib, self.lib.lp_rig_reset(self.rig))
 
     def close(self):
         if self.rig:

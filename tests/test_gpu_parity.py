@@ -584,6 +584,30 @@ def test_mask_reuse_across_cached_frames(lp, orc, in_flight):
 
 
 @pytest.mark.gpu
+def test_rig_reset_is_a_fresh_engine(lp, orc):
+    """lp_rig_reset (the drop-in engine's rig pool): after a reset the rig
+    forgets its HomographyCache, so frames of another scene estimate again
+    from frame 0 and equal the oracle's fresh engine, with up to 3 in flight."""
+    from paper_1810_03988_b200 import Rig
+    p = orc.default_params()
+    p.seed = p.matching.seed = 42
+    p.homography_refresh = 1 << 30
+    first = orc.planted_pair(480, 270, 0.25, 7)[:2]
+    second = orc.planted_pair(480, 270, 0.35, 8)[:2]
+    rig = Rig(lp, 2, 480, 270, p)
+    hs = [rig.submit_frame(list(first), t) for t in range(3)]
+    for h in hs:
+        rig.wait_frame(h)
+    rig.reset()
+    want = orc.stitch_frame(list(second), p, frame_index=0)
+    got = [rig.wait_frame(rig.submit_frame(list(second), t)) for t in range(2)]
+    for g in got:
+        assert g["canvas"] == want["canvas"]
+        assert np.array_equal(g["homographies"], want["homographies"])
+        assert np.array_equal(g["panorama"], want["panorama"])
+
+
+@pytest.mark.gpu
 def test_concurrent_rigs_threads(lp, orc):
     """Independent rigs on one context, driven from host threads (the config-5
     shape): each rig has its own stage stream, so their frames overlap on the
