@@ -25,3 +25,24 @@ for _ in range(50):
         h2.copy_(d2, non_blocking=True)
 torch.cuda.synchronize()
 print(f"both directions at once: {2 * 50 * n / (time.perf_counter() - t) / 1e9:.1f} GB/s total")
+
+# the same volumes split across several streams (one copy engine each?)
+for nsplit in (2, 4):
+    hs = [torch.empty(n // nsplit, dtype=torch.uint8).pin_memory() for _ in range(nsplit)]
+    ds = [torch.empty(n // nsplit, dtype=torch.uint8, device="cuda") for _ in range(nsplit)]
+    hs2 = [torch.empty(n // nsplit, dtype=torch.uint8).pin_memory() for _ in range(nsplit)]
+    ds2 = [torch.empty(n // nsplit, dtype=torch.uint8, device="cuda") for _ in range(nsplit)]
+    ss = [torch.cuda.Stream() for _ in range(2 * nsplit)]
+    for name, both in (("H2D", False), ("H2D+D2H", True)):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(50):
+            for i in range(nsplit):
+                with torch.cuda.stream(ss[i]):
+                    ds[i].copy_(hs[i], non_blocking=True)
+                if both:
+                    with torch.cuda.stream(ss[nsplit + i]):
+                        hs2[i].copy_(ds2[i], non_blocking=True)
+        torch.cuda.synchronize()
+        vol = (2 if both else 1) * 50 * (n // nsplit) * nsplit
+        print(f"{name} split over {nsplit} streams: {vol / (time.perf_counter() - t) / 1e9:.1f} GB/s")
