@@ -584,6 +584,30 @@ def test_mask_reuse_across_cached_frames(lp, orc, in_flight):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("w,h,ncams,overlap", [(333, 251, 2, 0.3), (257, 190, 3, 0.3), (641, 479, 3, 0.25)])
+def test_odd_frame_sizes_through_the_rig(lp, orc, w, h, ncams, overlap):
+    """Frame sizes that are not multiples of the compositor's alignment (the
+    generic blend kernel at some levels, cp.async staging at canvas edges,
+    ragged last tiles) through the rig with 3 frames in flight; the cached
+    frames reuse their seam masks. Every frame against the oracle."""
+    from paper_1810_03988_b200 import Rig
+    p = orc.default_params()
+    p.seed = p.matching.seed = 42
+    p.homography_refresh = 1 << 30
+    cams, _, _ = chain_cameras(orc, ncams, w, h, overlap, 11)
+    want = orc.stitch_frame(cams, p, frame_index=0)
+    rig = Rig(lp, ncams, w, h, p)
+    hs = [rig.submit_frame(list(cams), t) for t in range(3)]
+    for hnd in hs:
+        g = rig.wait_frame(hnd)
+        assert g["canvas"] == want["canvas"]
+        assert np.array_equal(g["homographies"], want["homographies"])
+        for c in range(ncams):
+            assert np.array_equal(g["keypoints"][c], want["keypoints"][c]), c
+        assert np.array_equal(g["panorama"], want["panorama"])
+
+
+@pytest.mark.gpu
 def test_rig_reset_is_a_fresh_engine(lp, orc):
     """lp_rig_reset (the drop-in engine's rig pool): after a reset the rig
     forgets its HomographyCache, so frames of another scene estimate again
