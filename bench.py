@@ -721,7 +721,15 @@ def main():
         # (lp_rig_submit / lp_rig_wait): every step's ingest copy, stages and
         # panorama egress are inside the timed region
         depth = int(os.environ.get("LPB_E2E_DEPTH", "3"))
-        host_sets = [[torch.from_numpy(c).pin_memory() for c in s] for s in sets[:2]]
+        # each set's cameras back to back in one page-locked block (one
+        # ingest copy per frame); LPB_E2E_CONTIG=0: one block per camera
+        if os.environ.get("LPB_E2E_CONTIG", "1") != "0":
+            host_sets = []
+            for st in sets[:2]:
+                blk = torch.from_numpy(np.ascontiguousarray(np.stack(st))).pin_memory()
+                host_sets.append([blk[c] for c in range(len(st))])
+        else:
+            host_sets = [[torch.from_numpy(c).pin_memory() for c in s] for s in sets[:2]]
         hpanos = [torch.empty(pano_cap, dtype=torch.uint8).pin_memory() for _ in range(depth)]
 
         def run_e2e(n, base):
