@@ -25,6 +25,7 @@ import subprocess
 import sys
 import tempfile
 import time
+import types
 
 import numpy as np
 
@@ -723,7 +724,22 @@ def main():
         depth = int(os.environ.get("LPB_E2E_DEPTH", "3"))
         # each set's cameras back to back in one page-locked block (one
         # ingest copy per frame); LPB_E2E_CONTIG=0: one block per camera
-        if os.environ.get("LPB_E2E_CONTIG", "1") != "0":
+        wc_blocks = []
+        if os.environ.get("LPB_E2E_WC", "0") == "1":
+            # write-combined page-locked blocks (lp_host_alloc_wc): written
+            # once here, read only by the device's copy engine
+            host_sets = []
+            for st in sets[:2]:
+                arr = np.ascontiguousarray(np.stack(st))
+                ptr = lib.lp_host_alloc_wc(arr.nbytes)
+                if not ptr:
+                    raise RuntimeError("lp_host_alloc_wc failed")
+                wc_blocks.append(ptr)
+                C.memmove(ptr, arr.ctypes.data, arr.nbytes)
+                fb = arr[0].nbytes
+                host_sets.append([types.SimpleNamespace(data_ptr=(lambda q: (lambda: q))(ptr + c * fb))
+                                  for c in range(len(st))])
+        elif os.environ.get("LPB_E2E_CONTIG", "1") != "0":
             host_sets = []
             for st in sets[:2]:
                 blk = torch.from_numpy(np.ascontiguousarray(np.stack(st))).pin_memory()
@@ -751,6 +767,8 @@ def main():
         if dist is not None:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         got = hpanos[(args.steps - 1) % depth][:canvas[0] * canvas[1]].to(torch.int64).sum().item()
+        for ptr in wc_blocks:
+            lib.lp_host_free(ptr)
         e2e = {"value": world * args.steps / float(tt.item()), "unit": "frames/s",
                "h2d_bytes_per_step": ncams * w * h, "d2h_bytes_per_step": canvas[0] * canvas[1],
                "timing": "wall clock around lp_rig_submit/lp_rig_wait (3 frames in flight) with pinned "

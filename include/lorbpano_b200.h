@@ -144,6 +144,10 @@ uint64_t lp_kernel_launches(void);
  * outputs there move by DMA asynchronously; pageable ones make the copy
  * synchronous with the host. NULL on failure. */
 void* lp_host_alloc(size_t bytes);
+/* The same, write-combined (cudaHostAllocWriteCombined): for frames the host
+ * writes once and only the device reads (not snooped during the copy in;
+ * slow for host reads). Freed with lp_host_free. */
+void* lp_host_alloc_wc(size_t bytes);
 void lp_host_free(void* p);
 
 /* ---- L-ORB primitives (lorb.hpp) ---- */

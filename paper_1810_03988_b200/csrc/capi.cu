@@ -362,6 +362,14 @@ void* lp_host_alloc(size_t bytes) {
     }
     return p;
 }
+void* lp_host_alloc_wc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, std::max<size_t>(bytes, 1), cudaHostAllocWriteCombined) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
 void lp_host_free(void* p) {
     if (p) cudaFreeHost(p);
 }

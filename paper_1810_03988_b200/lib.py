@@ -69,6 +69,12 @@ def load():
         lib.lp_rig_set_egress.restype = C.c_int
         lib.lp_rig_destroy.argtypes = [P]
         lib.lp_rig_destroy.restype = None
+        lib.lp_host_alloc.argtypes = [C.c_size_t]
+        lib.lp_host_alloc.restype = P
+        lib.lp_host_alloc_wc.argtypes = [C.c_size_t]
+        lib.lp_host_alloc_wc.restype = P
+        lib.lp_host_free.argtypes = [P]
+        lib.lp_host_free.restype = None
         lib.lp_rig_stitch.argtypes = [P, P, C.c_uint64, C.POINTER(abi.FrameOut)]
         lib.lp_rig_stitch.restype = C.c_int
         lib.lp_rig_panorama_capacity.argtypes = [P]
