@@ -305,6 +305,13 @@ lp_status lp_rig_create(lp_ctx* ctx, int ncams, int w, int h, const lp_params* p
 lp_status lp_rig_create_layout(lp_ctx* ctx, int ncams, int w, int h, const lp_camera* cams,
                                const lp_params* params, lp_rig** out);
 void lp_rig_destroy(lp_rig* rig);
+/* A frame whose panorama did not fit the caller's buffer (pano_cap) is still
+ * stitched: lp_rig_wait / lp_rig_wait_frame deliver everything else (the
+ * canvas included) and return LP_CAPACITY_OVERFLOW; the panorama stays in
+ * the frame's slot until the slot's next frame, and this copies it into dst
+ * (host or device, cap bytes; the reference's BufferPool grows for such
+ * canvases, pipeline.hpp:68-109). */
+lp_status lp_rig_copy_panorama(lp_rig* rig, uint64_t ticket, uint8_t* dst, size_t cap);
 /* A new StitchEngine's state on an existing rig (pipeline.hpp:343-350 with
  * the same layout and parameters): waits for the frames in flight, then
  * forgets the cached homographies (HomographyCache empty again) and every

@@ -715,6 +715,47 @@ int ref_run_engine_out(int ncams, int w, int h, const lp_params* params,
     });
 }
 
+// The reference's StitchEngine (Serial) over a sequence of frames
+// (images[f * ncams + c]): frame f's composite into panos + f * pano_stride
+// with its dims in dims[2f], dims[2f+1], or dropped[f] = 1 when the engine
+// dropped it (pipeline.hpp run_stage -> Metrics::drops). Sequence parity
+// tests compare the device rig against it frame by frame (HomographyCache
+// fallbacks and drops included).
+int ref_run_sequence(int ncams, int w, int h, const lp_params* params, const std::uint8_t* const* images,
+                     int nframes, std::uint8_t* panos, std::size_t pano_stride, int* dims, int* dropped) {
+    return guard([&] {
+        PipelineConfig pc;
+        pc.mode = PipelineMode::Serial;
+        pc.homography_refresh = params->homography_refresh;
+        StitchEngine eng(rig_layout(ncams, params->overlap_fraction), stitch_params(params), pc);
+        int produced = 0;
+        FrameSource src = [&]() -> std::optional<std::vector<ImageU8>> {
+            if (produced >= nframes) return std::nullopt;
+            std::vector<ImageU8> cams;
+            for (int c = 0; c < ncams; ++c)
+                cams.push_back(u8_image(images[static_cast<std::size_t>(produced) * ncams + c], w, h, 1));
+            ++produced;
+            return cams;
+        };
+        std::string sink_err;
+        FrameSink sink = [&](const FramePacket& pk) {
+            const std::uint64_t f = pk.frame_index;
+            if (pk.composite.data.size() > pano_stride) {
+                sink_err = "panorama capacity";
+                return;
+            }
+            std::memcpy(panos + f * pano_stride, pk.composite.data.data(), pk.composite.data.size());
+            dims[2 * f] = pk.composite.width;
+            dims[2 * f + 1] = pk.composite.height;
+        };
+        for (int f = 0; f < nframes; ++f) dropped[f] = 0;
+        Metrics m = eng.run(src, sink);
+        if (!sink_err.empty()) throw CapacityOverflow(sink_err);
+        for (const DroppedFrame& d : m.drops)
+            if (d.frame_index < static_cast<std::uint64_t>(nframes)) dropped[d.frame_index] = 1;
+    });
+}
+
 // nthreads independent serial engines, each running `frames_per_thread`
 // frames (SURVEY §8(d) mode iii). Returns aggregate frames/s.
 int ref_run_engines_parallel(int ncams, int w, int h, const lp_params* params,

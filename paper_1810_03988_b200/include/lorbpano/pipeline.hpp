@@ -987,7 +987,15 @@ private:
         FramePacket& p = *f.pkt;
         if (f.ticket != 0 && !p.failed) {
             const std::int64_t t0 = detail::now_ns();
-            const lp_status st = lp_rig_wait_frame(rig_, f.ticket, &f.out);
+            lp_status st = lp_rig_wait_frame(rig_, f.ticket, &f.out);
+            if (st == LP_CAPACITY_OVERFLOW && f.out.canvas.width > 0 && f.out.canvas.height > 0) {
+                // a canvas beyond the staging (the reference's BufferPool
+                // grows for it, pipeline.hpp:68-109): grow and fetch it
+                const std::size_t need = static_cast<std::size_t>(f.out.canvas.width) * f.out.canvas.height;
+                f.out.panorama = f.pano.get<std::uint8_t>(need);
+                f.out.pano_cap = need;
+                st = lp_rig_copy_panorama(rig_, f.ticket, f.out.panorama, need);
+            }
             const std::int64_t t1 = detail::now_ns();
             prof_[2] += t1 - t0;
             if (st != LP_OK) {

@@ -103,6 +103,8 @@ def load():
         lib.lp_rig_work_reset.restype = C.c_int
         lib.lp_rig_reset.argtypes = [P]
         lib.lp_rig_reset.restype = C.c_int
+        lib.lp_rig_copy_panorama.argtypes = [P, C.c_uint64, P, C.c_size_t]
+        lib.lp_rig_copy_panorama.restype = C.c_int
         lib.lp_profile_enable.argtypes = [C.c_int]
         lib.lp_profile_enable.restype = None
         lib.lp_profile_reset.argtypes = []
@@ -325,7 +327,17 @@ class Rig:
         return st
 
     def wait_frame(self, st):
-        _check(self.lib, self.lib.lp_rig_wait_frame(self.rig, st["ticket"], C.byref(st["fo"])))
+        code = self.lib.lp_rig_wait_frame(self.rig, st["ticket"], C.byref(st["fo"]))
+        fo = st["fo"]
+        if code == 24 and fo.canvas.width > 0 and fo.canvas.height > 0:
+            # the canvas outgrew the panorama buffer: the frame is stitched,
+            # its panorama waits in the rig (lp_rig_copy_panorama)
+            need = fo.canvas.width * fo.canvas.height
+            st["pano"] = np.zeros(need, np.uint8)
+            fo.panorama = st["pano"].ctypes.data_as(abi.c_u8p)
+            fo.pano_cap = need
+            code = self.lib.lp_rig_copy_panorama(self.rig, st["ticket"], st["pano"].ctypes.data, need)
+        _check(self.lib, code)
         return self._result(st)
 
 

@@ -3,6 +3,8 @@ oracle on identical seeded inputs. Integer/byte/index outputs and the FP32
 rasters must be bit-identical; homographies are compared bit-exact too (the
 device DLT replays the oracle's canonical SVD) with the reference's own
 tolerance (frobenius_rel < 1e-4, test_homography.cpp:12-19) as the floor."""
+import os
+
 import numpy as np
 import pytest
 
@@ -605,6 +607,82 @@ def test_odd_frame_sizes_through_the_rig(lp, orc, w, h, ncams, overlap):
         for c in range(ncams):
             assert np.array_equal(g["keypoints"][c], want["keypoints"][c]), c
         assert np.array_equal(g["panorama"], want["panorama"])
+
+
+def _ref_sequence(ref, frames, p):
+    """The reference's own StitchEngine (Serial) over the frame sequence:
+    every frame's composite, or None where the engine dropped it."""
+    import ctypes as C
+    nf, ncams = len(frames), len(frames[0])
+    h, w = frames[0][0].shape
+    flat = [np.ascontiguousarray(im) for fr in frames for im in fr]
+    arr = (C.c_void_p * len(flat))(*[im.ctypes.data for im in flat])
+    stride = 64 * ncams * w * h  # room for canvases far beyond BufferPool's ncams x w x 2h
+    panos = np.zeros((nf, stride), np.uint8)
+    dims = np.zeros(2 * nf, np.int32)
+    dropped = np.zeros(nf, np.int32)
+    fn = ref.lib.ref_run_sequence
+    fn.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_size_t,
+                   C.c_void_p, C.c_void_p]
+    st = fn(ncams, w, h, C.byref(p), arr, nf, panos.ctypes.data, stride, dims.ctypes.data, dropped.ctypes.data)
+    assert st == 0, ref.lib.ref_last_error().decode()
+    out = []
+    for f in range(nf):
+        if dropped[f]:
+            out.append(None)
+        else:
+            cw, ch = int(dims[2 * f]), int(dims[2 * f + 1])
+            out.append(panos[f, :cw * ch].reshape(ch, cw))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", range(int(os.environ.get("LPB_SOAK_CASES", "12"))))
+def test_randomised_rig_sequences_vs_reference_engine(lp, ref, case):
+    """Soak against the reference's own StitchEngine run over the same frame
+    sequence (oracle/_ref, Serial mode): random frame size, camera count,
+    overlap, refresh interval and frames in flight; the scene's overlap
+    changes every other frame, so re-registrations move the canvas (repairs),
+    estimates fail on some frames (the reference drops those without a cache
+    and falls back to the cache with one), and cached frames keep or rebuild
+    their arenas and seam masks. Every panorama and every drop must match."""
+    from paper_1810_03988_b200 import Rig, abi
+    rng = np.random.default_rng(1000 + case)
+    w, h = int(rng.integers(200, 520)), int(rng.integers(160, 360))
+    ncams = int(rng.integers(2, 4))
+    refresh = int(rng.choice([1, 2, 3, 1 << 30]))
+    in_flight = int(rng.integers(1, 4))
+    ovs = [float(rng.uniform(0.25, 0.4)), float(rng.uniform(0.25, 0.4))]
+    p = ref.default_params()
+    p.seed = p.matching.seed = 42 + case
+    p.homography_refresh = refresh
+    frames = [chain_cameras(ref, ncams, w, h, ovs[(t // 2) % 2], 50 + case * 10 + t)[0] for t in range(8)]
+    want = _ref_sequence(ref, frames, p)
+    rig = Rig(lp, ncams, w, h, p)
+    got, pending = {}, []
+
+    def land(t0, hnd):
+        try:
+            got[t0] = rig.wait_frame(hnd)["panorama"]
+        except abi.LorbError:
+            got[t0] = None
+
+    for t, cams in enumerate(frames):
+        try:
+            pending.append((t, rig.submit_frame(list(cams), t)))
+        except abi.LorbError:
+            got[t] = None
+        if len(pending) >= in_flight:
+            land(*pending.pop(0))
+    for t0, hnd in pending:
+        land(t0, hnd)
+    for t in range(len(frames)):
+        ctx = (case, w, h, ncams, refresh, in_flight, t)
+        if want[t] is None:
+            assert got[t] is None, ctx
+        else:
+            assert got[t] is not None, ctx
+            assert np.array_equal(got[t], want[t]), ctx
 
 
 @pytest.mark.gpu
