@@ -686,6 +686,71 @@ def test_randomised_rig_sequences_vs_reference_engine(lp, ref, case):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("case", range(int(os.environ.get("LPB_SOAK_CASES", "12"))))
+def test_randomised_parameters_vs_reference_engine(lp, ref, case):
+    """Soak over the parameter space (FAST threshold and arc, Harris sigma
+    and threshold, top_n, descriptor length, blur sigma, LSH tables / bits /
+    probes, ratio, PROSAC threshold / iterations / sampling, blend levels,
+    overlap fraction), each case a 5-frame sequence through the rig and
+    through the reference's own StitchEngine: every panorama and every drop
+    equal, and a parameter set the reference rejects is rejected by the rig
+    with the same status."""
+    from paper_1810_03988_b200 import Rig, abi
+    rng = np.random.default_rng(5000 + case)
+    w, h = int(rng.integers(240, 480)), int(rng.integers(180, 320))
+    ncams = int(rng.integers(2, 4))
+    p = ref.default_params()
+    p.seed = p.matching.seed = int(rng.integers(1, 1 << 30))
+    e = p.extraction
+    e.fast_threshold = int(rng.integers(10, 40))
+    e.fast_arc = int(rng.choice([9, 10, 12]))
+    e.harris_sigma = float(rng.choice([0.8, 1.0, 1.4, 2.0]))
+    e.top_n = int(rng.choice([100, 200, 500, 800]))
+    e.n_d = int(rng.choice([256, 512]))
+    e.brief_blur_sigma = float(rng.choice([1.5, 2.0, 3.0]))
+    m = p.matching
+    m.tables = int(rng.integers(2, 8))
+    m.bits = int(rng.choice([12, 16, 20]))
+    m.t_probes = int(rng.integers(0, 3))
+    m.ratio = float(rng.uniform(0.7, 0.9))
+    pr = p.prosac
+    pr.threshold_px = float(rng.choice([2.0, 3.0, 4.0]))
+    pr.max_iter = int(rng.choice([200, 1000, 2000]))
+    pr.sampling = int(rng.integers(0, 2))
+    p.blend_levels = int(rng.integers(1, 6))
+    p.homography_refresh = int(rng.choice([1, 2, 1 << 30]))
+    ov = float(rng.uniform(0.25, 0.4))
+    p.overlap_fraction = ov
+    frames = [chain_cameras(ref, ncams, w, h, ov, 70 + case * 10 + t)[0] for t in range(5)]
+    try:
+        want = _ref_sequence(ref, frames, p)
+    except AssertionError as err:  # the reference rejected the parameters
+        with pytest.raises(abi.LorbError):
+            rig = Rig(lp, ncams, w, h, p)
+            rig.wait_frame(rig.submit_frame(list(frames[0]), 0))
+        return
+    try:
+        rig = Rig(lp, ncams, w, h, p)
+    except abi.LorbError as err:
+        # the C-ABI rejects at creation what the reference's engine rejects
+        # in a stage of every frame (each frame dropped; the drop-in
+        # pipeline.hpp creates the rig inside its stage and drops them too)
+        assert err.name == "BadParams" and all(x is None for x in want), (case, str(err))
+        return
+    for t, cams in enumerate(frames):
+        try:
+            g = rig.wait_frame(rig.submit_frame(list(cams), t))["panorama"]
+        except abi.LorbError:
+            g = None
+        ctx = (case, w, h, ncams, t)
+        if want[t] is None:
+            assert g is None, ctx
+        else:
+            assert g is not None, ctx
+            assert np.array_equal(g, want[t]), ctx
+
+
+@pytest.mark.gpu
 def test_rig_reset_is_a_fresh_engine(lp, orc):
     """lp_rig_reset (the drop-in engine's rig pool): after a reset the rig
     forgets its HomographyCache, so frames of another scene estimate again
