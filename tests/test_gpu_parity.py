@@ -648,8 +648,11 @@ def test_randomised_rig_sequences_vs_reference_engine(lp, ref, case):
     their arenas and seam masks. Every panorama and every drop must match."""
     from paper_1810_03988_b200 import Rig, abi
     rng = np.random.default_rng(1000 + case)
-    w, h = int(rng.integers(200, 520)), int(rng.integers(160, 360))
-    ncams = int(rng.integers(2, 4))
+    # LPB_SOAK_BIG=1: frames up to 1280 x 720 and up to 4 cameras (slower reference)
+    big = os.environ.get("LPB_SOAK_BIG") == "1"
+    w, h = (int(rng.integers(600, 1280)), int(rng.integers(400, 720))) if big else \
+        (int(rng.integers(200, 520)), int(rng.integers(160, 360)))
+    ncams = int(rng.integers(2, 5 if big else 4))
     refresh = int(rng.choice([1, 2, 3, 1 << 30]))
     in_flight = int(rng.integers(1, 4))
     ovs = [float(rng.uniform(0.25, 0.4)), float(rng.uniform(0.25, 0.4))]
