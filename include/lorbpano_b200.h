@@ -1,7 +1,7 @@
 /* lorbpano_b200.h — C-ABI of the B200-native stitching hot path.
  *
  * This is the drop-in boundary under the reference's C++ API
- * (/root/reference/proj/include/lorbpano/*.hpp). Every entry point names the
+ * (/root/reference/proj/include/lorbpano/ headers). Every entry point names the
  * reference function it replaces (file:line, relative to proj/include/lorbpano/).
  * The C++ drop-in headers (paper_1810_03988_b200/include/lorbpano/) forward to
  * these functions and re-throw lp_status codes as the matching lorbpano::Error
