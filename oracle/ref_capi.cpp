@@ -721,13 +721,14 @@ int ref_run_engine_out(int ncams, int w, int h, const lp_params* params,
 // dropped it (pipeline.hpp run_stage -> Metrics::drops). Sequence parity
 // tests compare the device rig against it frame by frame (HomographyCache
 // fallbacks and drops included).
-int ref_run_sequence(int ncams, int w, int h, const lp_params* params, const std::uint8_t* const* images,
-                     int nframes, std::uint8_t* panos, std::size_t pano_stride, int* dims, int* dropped) {
-    return guard([&] {
+static void run_sequence(const RigLayout& layout, int ncams, int w, int h, const lp_params* params,
+                         const std::uint8_t* const* images, int nframes, std::uint8_t* panos, std::size_t pano_stride,
+                         int* dims, int* dropped) {
+    {
         PipelineConfig pc;
         pc.mode = PipelineMode::Serial;
         pc.homography_refresh = params->homography_refresh;
-        StitchEngine eng(rig_layout(ncams, params->overlap_fraction), stitch_params(params), pc);
+        StitchEngine eng(layout, stitch_params(params), pc);
         int produced = 0;
         FrameSource src = [&]() -> std::optional<std::vector<ImageU8>> {
             if (produced >= nframes) return std::nullopt;
@@ -753,6 +754,22 @@ int ref_run_sequence(int ncams, int w, int h, const lp_params* params, const std
         if (!sink_err.empty()) throw CapacityOverflow(sink_err);
         for (const DroppedFrame& d : m.drops)
             if (d.frame_index < static_cast<std::uint64_t>(nframes)) dropped[d.frame_index] = 1;
+    }
+}
+int ref_run_sequence(int ncams, int w, int h, const lp_params* params, const std::uint8_t* const* images,
+                     int nframes, std::uint8_t* panos, std::size_t pano_stride, int* dims, int* dropped) {
+    return guard([&] {
+        run_sequence(rig_layout(ncams, params->overlap_fraction), ncams, w, h, params, images, nframes, panos,
+                     pano_stride, dims, dropped);
+    });
+}
+// the same over a RigLayout (pre-transforms and crops, pipeline.hpp:240-247)
+int ref_run_sequence_layout(int ncams, int w, int h, const lp_camera* cams, const lp_params* params,
+                            const std::uint8_t* const* images, int nframes, std::uint8_t* panos,
+                            std::size_t pano_stride, int* dims, int* dropped) {
+    return guard([&] {
+        run_sequence(rig_layout_cams(ncams, params->overlap_fraction, cams), ncams, w, h, params, images, nframes,
+                     panos, pano_stride, dims, dropped);
     });
 }
 

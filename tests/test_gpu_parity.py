@@ -609,9 +609,10 @@ def test_odd_frame_sizes_through_the_rig(lp, orc, w, h, ncams, overlap):
         assert np.array_equal(g["panorama"], want["panorama"])
 
 
-def _ref_sequence(ref, frames, p):
-    """The reference's own StitchEngine (Serial) over the frame sequence:
-    every frame's composite, or None where the engine dropped it."""
+def _ref_sequence(ref, frames, p, cameras=None):
+    """The reference's own StitchEngine (Serial) over the frame sequence
+    (over a RigLayout when `cameras` are given): every frame's composite, or
+    None where the engine dropped it."""
     import ctypes as C
     nf, ncams = len(frames), len(frames[0])
     h, w = frames[0][0].shape
@@ -621,10 +622,19 @@ def _ref_sequence(ref, frames, p):
     panos = np.zeros((nf, stride), np.uint8)
     dims = np.zeros(2 * nf, np.int32)
     dropped = np.zeros(nf, np.int32)
-    fn = ref.lib.ref_run_sequence
-    fn.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_size_t,
-                   C.c_void_p, C.c_void_p]
-    st = fn(ncams, w, h, C.byref(p), arr, nf, panos.ctypes.data, stride, dims.ctypes.data, dropped.ctypes.data)
+    if cameras is None:
+        fn = ref.lib.ref_run_sequence
+        fn.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_size_t,
+                       C.c_void_p, C.c_void_p]
+        st = fn(ncams, w, h, C.byref(p), arr, nf, panos.ctypes.data, stride, dims.ctypes.data,
+                dropped.ctypes.data)
+    else:
+        fn = ref.lib.ref_run_sequence_layout
+        fn.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                       C.c_size_t, C.c_void_p, C.c_void_p]
+        cams = ref.cameras(cameras)
+        st = fn(ncams, w, h, cams, C.byref(p), arr, nf, panos.ctypes.data, stride, dims.ctypes.data,
+                dropped.ctypes.data)
     assert st == 0, ref.lib.ref_last_error().decode()
     out = []
     for f in range(nf):
@@ -740,6 +750,48 @@ def test_randomised_parameters_vs_reference_engine(lp, ref, case):
         # pipeline.hpp creates the rig inside its stage and drops them too)
         assert err.name == "BadParams" and all(x is None for x in want), (case, str(err))
         return
+    for t, cams in enumerate(frames):
+        try:
+            g = rig.wait_frame(rig.submit_frame(list(cams), t))["panorama"]
+        except abi.LorbError:
+            g = None
+        ctx = (case, w, h, ncams, t)
+        if want[t] is None:
+            assert g is None, ctx
+        else:
+            assert g is not None, ctx
+            assert np.array_equal(g, want[t]), ctx
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", range(int(os.environ.get("LPB_SOAK_CASES", "12")) // 2))
+def test_randomised_layout_sequences_vs_reference_engine(lp, ref, case):
+    """Soak over RigLayouts: per-camera pre-transforms (small rotations,
+    shears, perspective terms) and crops, stitched through lp_rig_create_layout
+    (stage_rectify_crop on ingest) and through the reference's own engine over
+    the same 5-frame sequence; every panorama and every drop equal."""
+    from paper_1810_03988_b200 import Rig, abi
+    rng = np.random.default_rng(9000 + case)
+    w, h = int(rng.integers(260, 520)), int(rng.integers(200, 360))
+    ncams = int(rng.integers(2, 4))
+    p = ref.default_params()
+    p.seed = p.matching.seed = 42 + case
+    p.homography_refresh = int(rng.choice([1, 2, 1 << 30]))
+    ov = float(rng.uniform(0.3, 0.4))
+    p.overlap_fraction = ov
+    specs = []
+    cw, ch = w - int(rng.integers(8, 24)), h - int(rng.integers(8, 24))  # one rectified size for all cameras
+    for c in range(ncams):
+        t = np.deg2rad(float(rng.uniform(-2.0, 2.0)))
+        co, si = np.cos(t), np.sin(t)
+        H = np.array([[co, -si, w / 2 - co * w / 2 + si * h / 2 + rng.uniform(-1, 1)],
+                      [si, co, h / 2 - si * w / 2 - co * h / 2 + rng.uniform(-1, 1)],
+                      [rng.uniform(-2e-5, 2e-5), rng.uniform(-2e-5, 2e-5), 1.0]])
+        x0, y0 = int(rng.integers(0, w - cw + 1)), int(rng.integers(0, h - ch + 1))
+        specs.append((H if rng.random() < 0.7 else None, (x0, y0, x0 + cw, y0 + ch)))
+    frames = [chain_cameras(ref, ncams, w, h, ov, 90 + case * 10 + t)[0] for t in range(5)]
+    want = _ref_sequence(ref, frames, p, cameras=specs)
+    rig = Rig(lp, ncams, w, h, p, cameras=specs)
     for t, cams in enumerate(frames):
         try:
             g = rig.wait_frame(rig.submit_frame(list(cams), t))["panorama"]
