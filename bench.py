@@ -5,8 +5,8 @@ Workload (default, BASELINE config 3): a 4-camera chain of 3840x2160 grayscale
 frames with 25% overlap, cached homographies (estimated on the first frame,
 homography_refresh = 2^30) and per-frame detect + describe + warp/blend, as
 the reference's StitchEngine runs it (pipeline.hpp:645-658). One step = one
-stitched frame. Inputs are synthetic (seeded uniform noise, sigma=1.5 blur,
-contrast stretch: the shape of synth::texture, synth.hpp:18-34), eight
+stitched frame. Inputs are synthetic: synth::texture (synth.hpp:17-34, the
+reference's own generator, byte-identical through lp_synth_texture), eight
 distinct frame sets rotate so the per-step input stream (8 x 33 MB) exceeds
 the 126 MB L2.
 
@@ -194,19 +194,10 @@ def run_streams(args, cfgd, lp, world, rank, local, dist):
 
 
 def texture(w, h, seed, sigma=1.5):
-    """synth::texture-shaped input (uniform noise, Gaussian blur, stretch)."""
-    rng = np.random.default_rng(seed)
-    noise = rng.integers(0, 256, size=(h, w)).astype(np.float32)
-    r = int(np.ceil(3 * sigma))
-    x = np.arange(-r, r + 1, dtype=np.float32)
-    k = np.exp(-(x * x) / (2 * sigma * sigma))
-    k /= k.sum()
-    pad = np.pad(noise, ((0, 0), (r, r)), mode="edge")
-    t = sum(k[i] * pad[:, i:i + w] for i in range(2 * r + 1))
-    pad = np.pad(t, ((r, r), (0, 0)), mode="edge")
-    b = sum(k[i] * pad[i:i + h, :] for i in range(2 * r + 1))
-    lo, hi = b.min(), b.max()
-    return np.clip(np.round((b - lo) * (255.0 / (hi - lo))), 0, 255).astype(np.uint8)
+    """synth::texture (synth.hpp:17-34), the reference's own input generator,
+    through the C-ABI's host restatement (lp_synth_texture, byte-identical)."""
+    from paper_1810_03988_b200.lib import synth_texture
+    return synth_texture(w, h, seed, sigma)
 
 
 def make_frame_sets(ncams, w, h, nsets, seed=42, overlap=0.25):

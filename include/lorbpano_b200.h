@@ -144,6 +144,10 @@ uint64_t lp_kernel_launches(void);
  * outputs there move by DMA asynchronously; pageable ones make the copy
  * synchronous with the host. NULL on failure. */
 void* lp_host_alloc(size_t bytes);
+/* synth::texture (synth.hpp:17-34): the reference's seeded test/bench input
+ * (mt19937_64 noise, gaussian_blur, contrast stretch), w x h u8 into out.
+ * Host only, byte-identical to the reference's. */
+lp_status lp_synth_texture(int w, int h, uint64_t seed, float sigma, uint8_t* out);
 /* The same, write-combined (cudaHostAllocWriteCombined): for frames the host
  * writes once and only the device reads (not snooped during the copy in;
  * slow for host reads). Freed with lp_host_free. */

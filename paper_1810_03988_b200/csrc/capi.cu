@@ -12,6 +12,7 @@
 
 #include <atomic>
 #include <cctype>
+#include <cmath>
 #include <chrono>
 #include <cstdio>
 #include <deque>
@@ -19,6 +20,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -362,6 +364,45 @@ void* lp_host_alloc(size_t bytes) {
     }
     return p;
 }
+// synth::texture (synth.hpp:17-34) on the host: the reference's seeded input
+// generator (mt19937_64 noise, gaussian_blur imgops.hpp:50-72 with
+// clamp-to-edge, contrast stretch, to_u8), so the bench and tools feed the
+// bytes the reference's own bench and tests feed
+lp_status lp_synth_texture(int w, int h, uint64_t seed, float sigma, uint8_t* out) {
+    return guard([&] {
+        if (w <= 0 || h <= 0 || !out) throw Status(LP_BAD_PARAMS, "synth_texture: empty image");
+        std::mt19937_64 rng(seed);
+        const size_t n = static_cast<size_t>(w) * h;
+        std::vector<float> noise(n), tmp(n), blur(n);
+        for (float& v : noise) v = static_cast<float>(rng() % 256);
+        const std::vector<float> k = host::gaussian_kernel(sigma);
+        const int r = static_cast<int>(k.size() / 2);
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x) {
+                float acc = 0.0f;
+                for (int i = -r; i <= r; ++i) acc += k[i + r] * noise[static_cast<size_t>(y) * w + std::clamp(x + i, 0, w - 1)];
+                tmp[static_cast<size_t>(y) * w + x] = acc;
+            }
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x) {
+                float acc = 0.0f;
+                for (int i = -r; i <= r; ++i) acc += k[i + r] * tmp[static_cast<size_t>(std::clamp(y + i, 0, h - 1)) * w + x];
+                blur[static_cast<size_t>(y) * w + x] = acc;
+            }
+        float lo = blur[0], hi = blur[0];
+        for (float v : blur) {
+            lo = std::min(lo, v);
+            hi = std::max(hi, v);
+        }
+        const float scale = hi > lo ? 255.0f / (hi - lo) : 0.0f;
+        for (size_t i = 0; i < n; ++i) {
+            float q = std::round((blur[i] - lo) * scale);  // to_u8, image.hpp:66-71
+            q = std::min(std::max(q, 0.0f), 255.0f);
+            out[i] = static_cast<uint8_t>(q);
+        }
+    });
+}
+
 void* lp_host_alloc_wc(size_t bytes) {
     void* p = nullptr;
     if (cudaHostAlloc(&p, std::max<size_t>(bytes, 1), cudaHostAllocWriteCombined) != cudaSuccess) {

@@ -75,6 +75,8 @@ def load():
         lib.lp_host_alloc_wc.restype = P
         lib.lp_host_free.argtypes = [P]
         lib.lp_host_free.restype = None
+        lib.lp_synth_texture.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_float, P]
+        lib.lp_synth_texture.restype = C.c_int
         lib.lp_rig_stitch.argtypes = [P, P, C.c_uint64, C.POINTER(abi.FrameOut)]
         lib.lp_rig_stitch.restype = C.c_int
         lib.lp_rig_panorama_capacity.argtypes = [P]
@@ -339,6 +341,14 @@ class Rig:
             code = self.lib.lp_rig_copy_panorama(self.rig, st["ticket"], st["pano"].ctypes.data, need)
         _check(self.lib, code)
         return self._result(st)
+
+
+def synth_texture(w, h, seed, sigma=1.5):
+    """synth::texture (synth.hpp:17-34) through the C-ABI (host only)."""
+    lib = load()
+    out = np.empty((h, w), np.uint8)
+    _check(lib, lib.lp_synth_texture(w, h, seed, sigma, out.ctypes.data))
+    return out
 
 
 def load_pnm(path):

@@ -67,3 +67,16 @@ def test_no_silent_cpu_fallback(lib):
     with pytest.raises(LorbError) as e:
         Lorb(0)
     assert e.value.name == "NoDevice"
+
+
+def test_synth_texture_is_the_references():
+    """lp_synth_texture (the bench's input generator) equals the reference's
+    synth::texture byte for byte (synth.hpp:17-34)."""
+    import numpy as np
+    from oracle import Oracle, ref_available
+    from paper_1810_03988_b200.lib import synth_texture
+    if not ref_available():
+        pytest.skip("reference oracle (oracle/_ref) not built here")
+    ref = Oracle("ref")
+    for w, h, seed, sigma in ((160, 120, 7, 1.5), (641, 479, 42, 1.5), (333, 251, 9, 2.0)):
+        assert np.array_equal(synth_texture(w, h, seed, sigma), ref.texture(w, h, seed, sigma))
