@@ -1228,6 +1228,7 @@ struct ComposeBuffers {
     ComposeArgs args{};
 
     DBuf runs, runs_used, status, mask_state;
+    size_t bytes_total = 0;  // device bytes of the windows and collapse buffers
     std::vector<float*> host_G, host_M;  // [c * levels + k]
     std::vector<PyrTma> pyr_tma;         // per source level k: k_pyr_down2's tensor maps
     std::vector<BlendTma> blend_tma;     // per level k < levels - 1: k_blend_lean's tensor maps
@@ -1255,8 +1256,10 @@ struct ComposeBuffers {
         }
         host_G.assign(static_cast<size_t>(ncams) * levels, nullptr);
         host_M.assign(host_G.size(), nullptr);
+        bytes_total = 0;
         auto alloc = [&](size_t bytes) {
             bufs.push_back(std::make_unique<DBuf>(std::max<size_t>(bytes, 16), s));
+            bytes_total += std::max<size_t>(bytes, 16);
             return bufs.back()->p;
         };
         size_t total_rows = 0;

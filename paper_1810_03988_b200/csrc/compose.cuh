@@ -213,6 +213,7 @@ struct GeomArgs {
     double* hinv;           // 9 * ncams, written only when the geometry could be derived
     GeomOutcome* out;       // host-mapped
     unsigned long long ticket;
+    int* skip;              // the slot's compositor skip word: 1 when this verdict does not fit the arenas
 };
 void geom_launch(const GeomArgs& a, cudaStream_t s);
 
@@ -261,6 +262,11 @@ struct ComposeArgs {
     // k_runs / k_mask0 / the mask half of k_pyr_down then skip. Null: always
     // recompute (caller-provided masks, LPB_MASK_REUSE=0)
     struct MaskState* mask_state;
+    // the slot's skip word (null: never): set by k_geom when the frame's
+    // device verdict does not fit the arenas it is composed on (the host
+    // recomposes it, repair), so the compositor's kernels exit at once;
+    // cleared after the frame by k_status_take
+    const int* skip;
     int hinv_base;                             // camera c's inverse map: c_hinv[hinv_base + c]
     uint8_t* out;                              // W[0] x H[0]
     int* status;
