@@ -46,6 +46,7 @@ constexpr int NX = TX + 2, NY = TY + 2;                 // response grid: tile +
 constexpr int HALO_MAX = kMaxHarrisR + 2;              // harris R + gradient 1 + NMS 1
 constexpr int IMG_MAX_X = TX + 2 * HALO_MAX, IMG_MAX_Y = TY + 2 * HALO_MAX;
 constexpr int GRAD_MAX_X = TX + 2 + 2 * kMaxHarrisR, GRAD_MAX_Y = TY + 2 + 2 * kMaxHarrisR;
+constexpr int GEN_DYN_SMEM = 2 * GRAD_MAX_X * GRAD_MAX_Y * static_cast<int>(sizeof(short));
 
 // survivors of the 3x3 NMS -> per-region key list (ballot-aggregated
 // atomics) and the first radix digit histogram of k_topn
@@ -88,8 +89,11 @@ __global__ void __launch_bounds__(256) k_detect(ExtractArgs a) {
     // integer central differences; the Harris loop forms the reference's exact
     // double (double(I(x+1)) - I(x-1)) / 2.0 (lorb.hpp:239-240) per tap
     __shared__ uint8_t s_img[IMG_MAX_X * IMG_MAX_Y];
-    __shared__ short s_gx[GRAD_MAX_X * GRAD_MAX_Y];
-    __shared__ short s_gy[GRAD_MAX_X * GRAD_MAX_Y];
+    // the two gradient planes (GEN_DYN_SMEM bytes) in dynamic shared memory:
+    // with them the static footprint would pass the 48 KB static limit
+    extern __shared__ __align__(16) short s_gdyn[];
+    short* s_gx = s_gdyn;
+    short* s_gy = s_gdyn + GRAD_MAX_X * GRAD_MAX_Y;
     __shared__ float s_resp[NX * NY];
     __shared__ short s_cand[NX * NY];
     __shared__ double s_w[(2 * kMaxHarrisR + 1) * (2 * kMaxHarrisR + 1)];
@@ -998,8 +1002,10 @@ void extract_launch(const ExtractArgs& a, cudaStream_t s) {
     LPB_CUDA(cudaMemsetAsync(a.hist, 0, sizeof(unsigned) * kTopnHistBins * a.nregions, s));
     if (a.max_tiles > 0) {
         // the local name keeps the profiler key "k_detect/0" for either instance
-        auto* k_detect = (a.harris_r == 3 && a.fast_arc == 9) ? &lpb::k_detect9 : &lpb::k_detect<0, 0>;
-        LPB_LAUNCH(k_detect, dim3(a.max_tiles, a.nregions), 256, 0, s, a);
+        const bool d9 = a.harris_r == 3 && a.fast_arc == 9;
+        auto* k_detect = d9 ? &lpb::k_detect9 : &lpb::k_detect<0, 0>;
+        if (!d9) ensure_dyn_smem(reinterpret_cast<const void*>(k_detect), GEN_DYN_SMEM);
+        LPB_LAUNCH(k_detect, dim3(a.max_tiles, a.nregions), 256, d9 ? 0 : GEN_DYN_SMEM, s, a);
     }
     if (a.top_n <= kTopnRankCap) {
         LPB_LAUNCH(k_topn, a.nregions, 1024, 0, s, a);
