@@ -158,7 +158,7 @@ def test_extract_widened_parameter_domain(lp, orc):
     path); beyond the two sigma bounds it raises BadParams (tested below)."""
     img = orc.texture(1920, 1080, 21)
     reg = [(20, 20, 1900, 1060, 0)]
-    for hs, bs, top_n in ((3.5, 2.0, 500), (1.0, 6.0, 300), (1.0, 2.0, 9000), (2.6, 5.5, 12000)):
+    for hs, bs, top_n in ((3.5, 2.0, 500), (4.0, 2.0, 500), (1.0, 6.0, 300), (1.0, 2.0, 9000), (2.6, 5.5, 12000)):
         cfg = orc.default_params().extraction
         cfg.harris_sigma, cfg.brief_blur_sigma, cfg.top_n = hs, bs, top_n
         pat = orc.brief_pattern(cfg.n_d, cfg.patch_half, 42)
