@@ -999,3 +999,47 @@ def test_rig_failed_frame_is_dropped_alone(lp, orc):
     # and the rig keeps working synchronously afterwards
     out = rig.stitch(list(frames[5]), 8)
     assert np.array_equal(out["panorama"], want[5])
+
+
+def test_rig_feature_fault_survives_repair(lp, orc):
+    """A frame whose feature stage fails and whose device verdict also moves
+    the canvas (so the rig recomposes it: repair) still fails at its wait():
+    the recomposition's status take must not overwrite the feature stage's
+    error with the recomposition's clean status. Inputs: the bench's config-1
+    style frame sets (the reference's synth::texture cut into two cameras, a
+    moving square per set), re-registered every frame, whose estimates give
+    canvases a pixel apart."""
+    from paper_1810_03988_b200 import LorbError, Rig
+    from paper_1810_03988_b200.lib import synth_texture
+    w, h, n = 640, 480, 16
+    shift = int(np.floor(w * 0.75 + 0.5))
+    wide = synth_texture(w + shift, h, 42)
+    size = max(4, h // 16)
+    frames = []
+    for s in range(8):
+        cams = [np.ascontiguousarray(wide[:, c * shift:c * shift + w]).copy() for c in range(2)]
+        px, py = (s * 7 * 37) % (w - size), (s * 3 * 37) % (h - size)
+        for c in range(2):
+            x0 = px - c * shift
+            if -size < x0 < w:
+                cams[c][py:py + size, max(0, x0):min(w, x0 + size)] = 255
+        frames.append(cams)
+    p = orc.default_params()
+    p.seed = p.matching.seed = 42
+    p.homography_refresh = 1
+    clean = Rig(lp, 2, w, h, p)
+    canv = [clean.stitch(list(frames[t % 8]), t)["canvas"] for t in range(n)]
+    moved = [t for t in range(2, n) if canv[t] != canv[t - 1]]
+    if not moved:
+        pytest.skip("no canvas jitter between these estimates")
+    bad = moved[0]
+    rig = Rig(lp, 2, w, h, p)
+    for t in range(bad):
+        assert rig.stitch(list(frames[t % 8]), t)["canvas"] == canv[t]
+    rig.inject_fault(bad, 10)  # LP_WINDOW_OUT_OF_BOUNDS in the feature stage of a repaired frame
+    with pytest.raises(LorbError) as e:
+        rig.stitch(list(frames[bad % 8]), bad)
+    assert e.value.name == "WindowOutOfBounds"
+    # the frames after it are unaffected
+    for t in range(bad + 1, min(bad + 4, n)):
+        assert rig.stitch(list(frames[t % 8]), t)["canvas"] == canv[t]
