@@ -379,8 +379,9 @@ lp_status lp_rig_set_egress(lp_rig* rig, int channels_rgb);
 size_t lp_rig_panorama_capacity(lp_rig* rig);
 /* The stream the rig's work is enqueued on (cudaStream_t). */
 void* lp_rig_stream(lp_rig* rig);
-/* Frame scheduler: 2 (default) runs extraction on a second stream concurrently
- * with warp/blend on cached-homography frames; 1 runs every stage in order. */
+/* Frame scheduler: 2 (default) runs each frame's extraction, matching and
+ * estimate on one of three rotating feature streams, concurrently with the
+ * compositor stream; 1 runs every stage in order on the rig stream. */
 lp_status lp_rig_set_streams(lp_rig* rig, int nstreams);
 /* Compositor launch chain replayed as a CUDA graph per frame slot (default
  * 1); 0 launches every kernel individually. */
