@@ -548,6 +548,39 @@ def test_async_reregistration_geometry_changes(lp, orc, in_flight):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("in_flight", [1, 3])
+def test_geometry_arenas_evicted_and_revisited(lp, orc, in_flight):
+    """The rig keeps the compositor arenas and graphs of its last six
+    geometries (LRU). Eight planted overlaps give eight canvases: cycling
+    through them evicts arenas, revisits kept ones and rebuilds evicted ones,
+    with frames in flight; every frame equals the oracle's."""
+    from paper_1810_03988_b200 import Rig
+    p = orc.default_params()
+    p.seed = p.matching.seed = 42
+    p.homography_refresh = 1
+    ovs = [0.22, 0.24, 0.26, 0.28, 0.30, 0.32, 0.34, 0.36]
+    order = [0, 1, 2, 3, 4, 5, 6, 7, 1, 7, 0, 4, 0, 2, 6, 6]
+    pairs = {i: orc.planted_pair(480, 270, ovs[i], 11)[:2] for i in set(order)}
+    rig = Rig(lp, 2, 480, 270, p)
+    got, inflight = {}, []
+    for t, i in enumerate(order):
+        inflight.append((t, rig.submit_frame(list(pairs[i]), t)))
+        if len(inflight) >= in_flight:
+            t0, hnd = inflight.pop(0)
+            got[t0] = rig.wait_frame(hnd)
+    for t0, hnd in inflight:
+        got[t0] = rig.wait_frame(hnd)
+    canvases = set()
+    for t, i in enumerate(order):
+        want = orc.stitch_frame(list(pairs[i]), p, frame_index=t)
+        g = got[t]
+        canvases.add(tuple(want["canvas"]))
+        assert g["canvas"] == want["canvas"], (t, g["canvas"], want["canvas"])
+        assert np.array_equal(g["panorama"], want["panorama"]), t
+    assert len(canvases) > 6, canvases
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("in_flight", [1, 3])
 def test_mask_reuse_across_cached_frames(lp, orc, in_flight):
     """Seam masks, coverage runs and the mask pyramid depend only on the
     inverse maps and windows, so frames composed on the maps of the previous
