@@ -202,6 +202,7 @@ void hinv_upload(int base, const double* src, int n, bool src_on_device, cudaStr
 struct GeomOutcome {
     unsigned long long ticket;
     int done, estimated, same, status;
+    int which;  // arenas the verdict fits: 0 the submit-time ones, 1 the alternate, -1 neither
     lp_homography H[kMaxCompCams];
 };
 struct GeomArgs {
@@ -214,6 +215,10 @@ struct GeomArgs {
     GeomOutcome* out;       // host-mapped
     unsigned long long ticket;
     int* skip;              // the slot's compositor skip word: 1 when this verdict does not fit the arenas
+    // an alternate kept geometry whose compositor is enqueued too (nullptr:
+    // none): its skip word is cleared only when the verdict fits it and not `ref`
+    const RigGeom* ref2;
+    int* skip2;
 };
 void geom_launch(const GeomArgs& a, cudaStream_t s);
 
