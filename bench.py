@@ -653,7 +653,11 @@ def main():
     pano_cap = rig.panorama_capacity()
     dpano = torch.empty(pano_cap, dtype=torch.uint8, device="cuda")
     fo = frame_out(dpano.data_ptr(), pano_cap)
-    dev_depth = int(os.environ.get("LPB_DEV_DEPTH", "1"))
+    # frames in flight in the device-resident loop: the pipelined API
+    # (lp_rig_submit / lp_rig_wait, 3 in flight) for cached-homography frames,
+    # lp_rig_stitch one frame at a time for re-registering ones (A/B on B200:
+    # cfg3 1714 -> 1755 at 3; cfg1/cfg2/cfg4 1-4 % faster at 1)
+    dev_depth = int(os.environ.get("LPB_DEV_DEPTH", "3" if args.config == "cfg3" else "1"))
     dpanos = [dpano] + [torch.empty(pano_cap, dtype=torch.uint8, device="cuda") for _ in range(dev_depth - 1)]
 
     def step(i):
@@ -816,7 +820,8 @@ def main():
                 "config": {"workload": cfgd["workload"], "cameras": ncams, "width": w, "height": h,
                            "canvas": list(canvas), "overlap": 0.25,
                            "l2": f"{nsets} rotating input frame sets ({nsets * ncams * w * h / 1e6:.0f} MB) > 126 MB L2",
-                           "parallelism": f"replicas x{world} (independent rigs, no data-path collective)"},
+                           "parallelism": f"replicas x{world} (independent rigs, no data-path collective)",
+                           "device_frames_in_flight": dev_depth},
                 "gpu_launches": int(launches), "clocks": clk, "roofline": roofline,
                 "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "stage_ms": stage_ms if not args.no_profile else None,
                 "frame_hbm": frame_hbm, "kernel_ms": stage, "rank_checksums": checksums}
