@@ -227,6 +227,7 @@ struct MaskState {
     int valid;  // this frame's maps equal `key`: every mask buffer is current
     int have;   // `key` holds the maps of the last compose that made the masks
     unsigned next_runs, next_mask0;  // k_runs / k_mask0 work counters (reset by k_warp)
+    unsigned runs_done;              // k_runs_mask0: run items finished (reset by k_warp)
     double key[kMaxCompCams][9];
 };
 
